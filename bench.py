@@ -1,0 +1,306 @@
+#!/usr/bin/env python
+"""Benchmark of the GNND hot path on B200 (BASELINE.json metric:
+"kNN-graph build sec at recall@10>=0.95 (SIFT1M, DEEP100M shape)").
+
+One step = one complete knng_build (init + all iterations + export, every
+SURVEY.md section 8(a) row of the build) over the SIFT1M-shaped workload
+(BASELINE.json configs[1]: 1M x 128 fp32, k = 32, L2), vectors resident in
+HBM.  The vectors (512 MB) exceed the 126 MB L2, so no L2 flush is needed
+between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Multi-GPU (torchrun, one process per GPU): every rank builds its own
+SIFT1M-shaped shard (independent problems, no collective; "scaling": weak).
+--impl reference times the oracle (oracle/, plain C, single thread) on a
+bounded sample of the same workload on the host CPU (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "kNN-graph build sec at recall@10>=0.95 (SIFT1M, DEEP100M shape), 1/2/4/8 B200"
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # derived
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--k", type=int, default=32)
+    ap.add_argument("--p", type=int, default=16)
+    ap.add_argument("--iters", type=int, default=8)
+    ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--recall-nodes", type=int, default=10_000)
+    ap.add_argument("--cpu-sample", type=int, default=20_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        return float(m["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def workload(args, rank):
+    import datagen
+    X = datagen.make("sift", args.n, seed=1 + rank)
+    return X
+
+
+def cpu_baseline(args, X) -> dict:
+    """The oracle as it stands, single thread, on a bounded sample of the
+    same workload: the first `cpu_sample` rows, same k/p/iters/seed; build
+    seconds extrapolated linearly in n (GNND's per-iteration work is
+    per-node: sample, 2p-bounded join, bounded update)."""
+    import oracle.oracle as orc
+    ns = min(args.cpu_sample, X.shape[0])
+    Xs = np.ascontiguousarray(X[:ns])
+    t0 = time.perf_counter()
+    orc.build(Xs, args.k, args.p, args.iters, args.seed)
+    dt = time.perf_counter() - t0
+    return {"value": dt * (X.shape[0] / ns), "unit": "s", "cores": 1, "kind": "oracle",
+            "sample": f"oracle GNND build of the first {ns} rows of the same SIFT1M-shaped workload "
+                      f"(k={args.k}, p={args.p}, iters={args.iters}) took {dt:.2f} s on 1 host core; "
+                      f"value = that x {X.shape[0]}/{ns} (linear in n)",
+            "sample_seconds": dt}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    X = workload(args, 0)
+    for _ in range(args.warmup):
+        pass  # the oracle has no warm-up state; warm-up steps are not repeated on the CPU
+    times = []
+    res = None
+    for _ in range(args.steps):
+        res = cpu_baseline(args, X)
+        times.append(res["value"])
+    v = statistics.median(times)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1000.0, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic GMM-LR SIFT-shaped (datagen 'sift', seed 1)",
+            "config": {"workload": "C2 SIFT1M-shaped", "n": args.n, "d": 128, "k": args.k,
+                       "sample_size": args.p, "iters": args.iters, "metric": "l2"},
+            "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "oracle", "sample": res["sample"]},
+            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_2103_15386_b200.knng as K
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    X = workload(args, rank)
+    n, d = X.shape
+    Xd = torch.from_numpy(X).cuda()
+    stream = torch.cuda.current_stream()
+    ws = torch.empty(K.knng_build_workspace_bytes(K.KNNG_F32, n, d, args.k, args.p), dtype=torch.uint8,
+                     device="cuda")
+    ids = torch.empty((n, args.k), dtype=torch.int32, device="cuda")
+    dists = torch.empty((n, args.k), dtype=torch.float32, device="cuda")
+
+    def step():
+        K.knng_build(Xd, args.k, args.iters, args.p, args.seed, "l2", ids, dists, ws, stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: device time with CUDA events on the launch stream
+    K.knng_set_timing(True)
+    K.knng_reset_timing()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = K.knng_launch_count()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    launches = K.knng_launch_count() - launches0
+    clk = clocks.stop()
+    K.knng_set_timing(False)
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    join_ms, join_launches = K.knng_kernel_time("k_join")
+    stats = K.knng_last_stats()
+
+    # ---- quality: recall@10 on sampled nodes vs exact brute force (GPU)
+    import datagen
+    q = datagen.sample_nodes(n, args.recall_nodes)
+    gi, gd = K.knng_bruteforce(Xd, torch.from_numpy(q), 10)
+    g_thr = gd[:, 9:10]
+    mine = dists[torch.from_numpy(q).cuda().long(), :10]
+    recall = float((mine <= g_thr).float().mean().item())
+
+    # ---- end to end through the public host API (pinned buffers, copies timed)
+    e2e = None
+    if not args.no_e2e:
+        Xh = torch.from_numpy(X).pin_memory()
+        ih = torch.empty((n, args.k), dtype=torch.int32).pin_memory()
+        dh = torch.empty((n, args.k), dtype=torch.float32).pin_memory()
+        lib = K.lib()
+
+        def e2e_step():
+            st = lib.knng_build_host(Xh.data_ptr(), K.KNNG_F32, n, d, args.k, K.KNNG_L2SQ, args.iters, args.p,
+                                     args.seed, ih.data_ptr(), dh.data_ptr(), stream.cuda_stream)
+            if st != 0:
+                raise RuntimeError(K.knng_last_error())
+
+        e2e_step()
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t0) / args.steps
+        if world > 1:
+            t = torch.tensor([e2e_s], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(X.nbytes),
+               "d2h_bytes_per_step": int(n * args.k * 8)}
+
+    # ---- roofline of the dominant kernel (k_join): algorithmic bytes
+    rows = sum(s["rows"] for s in stats)
+    evals = sum(s["dist_evals"] for s in stats)
+    alg_bytes_per_launch = rows * (d * 4 + 4) / max(1, len(stats))
+    join_avg_ms = join_ms / max(1, join_launches)
+    achieved_gbs = alg_bytes_per_launch / (join_avg_ms * 1e-3) / 1e9 if join_avg_ms > 0 else 0.0
+    peak, peak_kind = peaks()
+    alu_tflops = evals * d * 3 / max(1, len(stats)) / (join_avg_ms * 1e-3) / 1e12 if join_avg_ms > 0 else 0.0
+    roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
+                "frac": achieved_gbs / peak, "traffic": None, "peak_source": peak_kind,
+                "kernel": "k_join", "avg_launch_ms": join_avg_ms, "launches": join_launches,
+                "share_of_step": join_ms / args.steps / ms if ms > 0 else None,
+                "alg_bytes_per_launch": alg_bytes_per_launch,
+                "alu": {"achieved_tflops": alu_tflops, "peak_tflops": FP32_PEAK_TFLOPS,
+                        "frac": alu_tflops / FP32_PEAK_TFLOPS, "flops_per_dim_pair": 3}}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args, X)
+        cpu.pop("sample_seconds", None)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": ms / 1000.0, "unit": "s", "n_gpus": world, "steps": args.steps,
+                "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic GMM-LR SIFT-shaped (datagen 'sift', seed 1+rank), integer-valued fp32",
+                "config": {"workload": "C2 SIFT1M-shaped (BASELINE.json configs[1])", "n": n, "d": d,
+                           "k": args.k, "sample_size": args.p, "iters": args.iters, "metric": "l2",
+                           "l2_flush": "inputs (512 MB) larger than L2", "per_rank": "one 1M build per GPU"},
+                "recall_at_10": recall, "recall_nodes": len(q),
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "clocks": clk,
+                "iter_stats": stats}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,220 @@
+// common.cuh -- shared device helpers of the GNND CUDA path (sm_100a).
+//
+// Nothing here is shared with oracle/: the Philox generator, the canonical
+// distance and the warp sorting networks below are this library's own.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace knng {
+
+constexpr uint64_t kSentinel = 0xFFFFFFFFFFFFFFFFull;  // (inf, inf) of Alg. 2
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+
+enum : uint32_t { kTagInit = 1, kTagRevNew = 2, kTagRevOld = 3, kTagMergeSeed = 4 };
+
+// key(d, id) = bits(d) << 32 | id  (d >= +0, so u64 order == (d, id) order)
+__device__ __forceinline__ uint64_t make_key(float d, uint32_t id) {
+    return (static_cast<uint64_t>(__float_as_uint(d)) << 32) | id;
+}
+__device__ __forceinline__ uint32_t key_id(uint64_t k) { return static_cast<uint32_t>(k); }
+__device__ __forceinline__ float key_dist(uint64_t k) {
+    return __uint_as_float(static_cast<uint32_t>(k >> 32));
+}
+
+// ---------------------------------------------------------------- Philox
+// Philox4x32-10 (Salmon et al. SC'11), multipliers 0xD2511F53 / 0xCD9E8D57,
+// Weyl key increments 0x9E3779B9 / 0xBB67AE85.
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 key) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c.x);
+        const uint32_t lo0 = 0xD2511F53u * c.x;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z);
+        const uint32_t lo1 = 0xCD9E8D57u * c.z;
+        c = make_uint4(hi1 ^ c.y ^ key.x, lo1, hi0 ^ c.w ^ key.y, lo0);
+        key.x += 0x9E3779B9u;
+        key.y += 0xBB67AE85u;
+    }
+    return c;
+}
+__device__ __forceinline__ uint2 seed_key(uint64_t seed) {
+    return make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
+}
+// uniform integer in [0, N): high 64 bits of (out.y:out.x) * N  (D31)
+__device__ __forceinline__ uint64_t uniform_below(uint4 o, uint64_t N) {
+    const uint64_t r = (static_cast<uint64_t>(o.y) << 32) | o.x;
+    return __umul64hi(r, N);
+}
+
+// ---------------------------------------------------------------- warp utils
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+__device__ __forceinline__ uint64_t shfl_u64(uint64_t v, int src) {
+    return __shfl_sync(kFull, v, src);
+}
+__device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
+    return __shfl_xor_sync(kFull, v, m);
+}
+
+// Bitonic sort of one u64 per lane, ascending across lanes 0..31.
+__device__ __forceinline__ uint64_t warp_sort_u64(uint64_t x) {
+    const uint32_t lane = lane_id();
+#pragma unroll
+    for (int k2 = 2; k2 <= 32; k2 <<= 1) {
+#pragma unroll
+        for (int j = k2 >> 1; j > 0; j >>= 1) {
+            const uint64_t o = shfl_xor_u64(x, j);
+            const bool up = (lane & k2) == 0;
+            const bool lower = (lane & j) == 0;
+            const uint64_t mn = o < x ? o : x, mx = o < x ? x : o;
+            x = (lower == up) ? mn : mx;
+        }
+    }
+    return x;
+}
+
+// Element of the list-merge network: key + meta (bit0 = NEW flag, bit1 =
+// origin: 0 list, 1 candidate).  Order (key, origin): a list entry sorts in
+// front of an equal-key candidate, so dedup keeps the list's flag (D16/D17).
+struct Elem {
+    uint64_t key;
+    uint32_t meta;
+};
+__device__ __forceinline__ bool elem_less(const Elem& a, const Elem& b) {
+    return a.key < b.key || (a.key == b.key && (a.meta >> 1) < (b.meta >> 1));
+}
+__device__ __forceinline__ Elem shfl_xor_elem(const Elem& e, int m) {
+    return Elem{shfl_xor_u64(e.key, m), __shfl_xor_sync(kFull, e.meta, m)};
+}
+__device__ __forceinline__ Elem shfl_elem(const Elem& e, int src) {
+    return Elem{shfl_u64(e.key, src), __shfl_sync(kFull, e.meta, src)};
+}
+__device__ __forceinline__ Elem warp_sort_elem(Elem x) {
+    const uint32_t lane = lane_id();
+#pragma unroll
+    for (int k2 = 2; k2 <= 32; k2 <<= 1) {
+#pragma unroll
+        for (int j = k2 >> 1; j > 0; j >>= 1) {
+            const Elem o = shfl_xor_elem(x, j);
+            const bool up = (lane & k2) == 0;
+            const bool lower = (lane & j) == 0;
+            const bool o_less = elem_less(o, x);
+            const bool take_o = (lower == up) ? o_less : !o_less && (o.key != x.key || o.meta != x.meta);
+            if (take_o) x = o;
+        }
+    }
+    return x;
+}
+// bitonic sequence across the warp -> ascending
+__device__ __forceinline__ Elem warp_bitonic_merge_elem(Elem x) {
+    const uint32_t lane = lane_id();
+#pragma unroll
+    for (int j = 16; j > 0; j >>= 1) {
+        const Elem o = shfl_xor_elem(x, j);
+        const bool lower = (lane & j) == 0;
+        const bool o_less = elem_less(o, x);
+        if (lower ? o_less : (!o_less && (o.key != x.key || o.meta != x.meta))) x = o;
+    }
+    return x;
+}
+
+// Merge one chunk of up to 32 candidate keys (one per lane, any order, may
+// repeat, kSentinel = empty) into a sorted unique list held one entry per
+// lane (lanes >= its length hold kSentinel).  Result: the 32 smallest unique
+// keys of the union, ascending; list entries keep their NEW flag, newcomers
+// are NEW.  scratch: 32 Elem of per-warp shared memory.  Returns the number
+// of newcomers that entered.
+__device__ __forceinline__ int warp_merge_chunk(Elem& cur, uint64_t cand, Elem* scratch) {
+    const uint32_t lane = lane_id();
+    Elem b{cand, 3u};  // origin = candidate, NEW
+    b = warp_sort_elem(b);
+    // half-cleaner of the 64-sequence cur[0..31] ++ reverse(b)
+    const Elem br = shfl_elem(b, 31 - lane);
+    Elem lo = elem_less(br, cur) ? br : cur;
+    Elem hi = elem_less(br, cur) ? cur : br;
+    lo = warp_bitonic_merge_elem(lo);
+    hi = warp_bitonic_merge_elem(hi);
+    // dedup adjacent equal keys over lo[0..31] ++ hi[0..31]
+    const uint64_t lo_prev = shfl_u64(lo.key, (lane + 31) & 31);
+    const uint64_t lo_last = shfl_u64(lo.key, 31);
+    const uint64_t hi_prev_raw = shfl_u64(hi.key, (lane + 31) & 31);
+    const uint64_t hi_prev = lane == 0 ? lo_last : hi_prev_raw;
+    const bool lo_ok = lo.key != kSentinel && (lane == 0 || lo.key != lo_prev);
+    const bool hi_ok = hi.key != kSentinel && hi.key != hi_prev;
+    const uint32_t lo_mask = __ballot_sync(kFull, lo_ok);
+    const uint32_t hi_mask = __ballot_sync(kFull, hi_ok);
+    const int lo_cnt = __popc(lo_mask);
+    const int r_lo = __popc(lo_mask & lanemask_lt());
+    const int r_hi = lo_cnt + __popc(hi_mask & lanemask_lt());
+    __syncwarp();
+    scratch[lane] = Elem{kSentinel, 0u};
+    __syncwarp();
+    if (lo_ok) scratch[r_lo] = lo;
+    if (hi_ok && r_hi < 32) scratch[r_hi] = hi;
+    __syncwarp();
+    cur = scratch[lane];
+    __syncwarp();
+    const bool entered = cur.key != kSentinel && (cur.meta >> 1) != 0;
+    cur.meta &= 1u;  // the merged list is all "list origin" from now on
+    return __popc(__ballot_sync(kFull, entered));
+}
+
+// ---------------------------------------------------------------- distances
+// Canonical distances (D5/D6): one thread owns one pair and accumulates the
+// dimensions in order 0..d-1: acc = fmaf(x_i - y_i, x_i - y_i, acc).
+template <typename T>
+struct Canon;
+
+template <>
+struct Canon<float> {
+    __device__ static __forceinline__ float l2(const float* __restrict__ a,
+                                               const float* __restrict__ b, int d) {
+        float acc = 0.0f;
+        if ((d & 3) == 0 && ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0) {
+            const float4* a4 = reinterpret_cast<const float4*>(a);
+            const float4* b4 = reinterpret_cast<const float4*>(b);
+            for (int i = 0; i < (d >> 2); ++i) {
+                const float4 x = __ldg(a4 + i), y = __ldg(b4 + i);
+                float t;
+                t = x.x - y.x; acc = fmaf(t, t, acc);
+                t = x.y - y.y; acc = fmaf(t, t, acc);
+                t = x.z - y.z; acc = fmaf(t, t, acc);
+                t = x.w - y.w; acc = fmaf(t, t, acc);
+            }
+        } else {
+            for (int i = 0; i < d; ++i) {
+                const float t = __ldg(a + i) - __ldg(b + i);
+                acc = fmaf(t, t, acc);
+            }
+        }
+        return acc;
+    }
+    // 1 - <x^, y^> on pre-normalised rows, clamped at +0 (D6)
+    __device__ static __forceinline__ float cos(const float* __restrict__ a,
+                                                const float* __restrict__ b, int d) {
+        float s = 0.0f;
+        for (int i = 0; i < d; ++i) s = fmaf(__ldg(a + i), __ldg(b + i), s);
+        const float r = 1.0f - s;
+        return r > 0.0f ? r : 0.0f;
+    }
+};
+
+template <>
+struct Canon<uint8_t> {
+    __device__ static __forceinline__ float l2(const uint8_t* __restrict__ a,
+                                               const uint8_t* __restrict__ b, int d) {
+        int acc = 0;
+        for (int i = 0; i < d; ++i) {
+            const int t = static_cast<int>(__ldg(a + i)) - static_cast<int>(__ldg(b + i));
+            acc += t * t;
+        }
+        return static_cast<float>(acc);
+    }
+};
+
+}  // namespace knng

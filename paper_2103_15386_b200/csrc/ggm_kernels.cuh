@@ -1,0 +1,92 @@
+// ggm_kernels.cuh -- GGM graph merge, Alg. 3.  Warp per node of
+// the combined set S = S1 U S2 (rows [0, nA) are S1, [nA, n) are S2).
+#pragma once
+#include "graph_kernels.cuh"
+
+namespace knng {
+
+// Seed (Alg. 3 lines 1-7): keep the first ceil(k/2)
+// entries of the node's input list (OLD), reserve the last floor(k/2)
+// (G^v), append floor(k/2) distinct ids of the other subset drawn
+// in counter order from Philox(MERGE_SEED, i, j, level) (D21), NEW,
+// then sort (D25).  Input lists must be ascending (as knng_build emits).
+template <typename T, bool COS>
+__global__ void k_ggm_seed(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, int64_t nA, int level,
+                           uint64_t seed, const uint32_t* __restrict__ idsA, const float* __restrict__ distsA,
+                           const uint32_t* __restrict__ idsB, const float* __restrict__ distsB, Graph G,
+                           uint64_t* __restrict__ reserved) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (i >= D.n) return;
+    const uint32_t lane = lane_id();
+    const int k = D.k, kh = (k + 1) / 2, kr = k - kh;
+    const bool own_b = i >= nA;
+    uint64_t in = kSentinel;
+    if (static_cast<int>(lane) < k) {
+        if (!own_b) {
+            in = make_key(distsA[static_cast<size_t>(i) * k + lane], idsA[static_cast<size_t>(i) * k + lane]);
+        } else {
+            const size_t o = static_cast<size_t>(i - nA) * k + lane;
+            in = make_key(distsB[o], static_cast<uint32_t>(idsB[o] + nA));
+        }
+    }
+    if (static_cast<int>(lane) >= kh && static_cast<int>(lane) < k)
+        reserved[static_cast<size_t>(i) * kr + (lane - kh)] = in;
+    // chosen ids: lanes [0, kh) keep their input entry; draws fill [kh, k)
+    uint32_t chosen = static_cast<int>(lane) < kh ? key_id(in) : 0xFFFFFFFFu;
+    const int64_t base = own_b ? 0 : nA;
+    const uint64_t size = static_cast<uint64_t>(own_b ? nA : D.n - nA);
+    const uint2 key = seed_key(seed);
+    int cnt = kh;
+    for (uint32_t j0 = 0; cnt < k; j0 += 32) {
+        const uint4 o = philox4x32_10(
+            make_uint4(kTagMergeSeed, static_cast<uint32_t>(i), j0 + lane, static_cast<uint32_t>(level)), key);
+        const uint32_t v = static_cast<uint32_t>(base + static_cast<int64_t>(uniform_below(o, size)));
+        bool dup = false;
+        for (int t = 0; t < cnt; ++t) dup |= (__shfl_sync(kFull, chosen, t) == v);
+        for (int l = 0; l < 32; ++l) {
+            const uint32_t vl = __shfl_sync(kFull, v, l);
+            dup |= (static_cast<uint32_t>(l) < lane && vl == v);
+        }
+        const uint32_t acc = __ballot_sync(kFull, !dup);
+        const int want = static_cast<int>(lane) - cnt;
+        const bool take = want >= 0 && want < __popc(acc) && static_cast<int>(lane) < k;
+        const int src = take ? static_cast<int>(__fns(acc, 0, want + 1)) : 0;
+        const uint32_t got = __shfl_sync(kFull, v, src);
+        if (take) chosen = got;
+        cnt = min(k, cnt + __popc(acc));
+    }
+    Elem e{kSentinel, 0u};
+    if (static_cast<int>(lane) < kh) {
+        e = Elem{in, 0u};  // kept half: OLD
+    } else if (static_cast<int>(lane) < k) {
+        float dist;
+        if constexpr (COS) {
+            dist = Canon<float>::cos(Xn + static_cast<size_t>(i) * D.d, Xn + static_cast<size_t>(chosen) * D.d, D.d);
+        } else {
+            dist = Canon<T>::l2(X + static_cast<size_t>(i) * D.d, X + static_cast<size_t>(chosen) * D.d, D.d);
+        }
+        e = Elem{make_key(dist, chosen), 1u};  // cross sample: NEW
+    }
+    e = warp_sort_elem(e);
+    const bool in_list = static_cast<int>(lane) < k;
+    if (in_list) G.keys[static_cast<size_t>(i) * k + lane] = e.key;
+    const uint32_t nm = __ballot_sync(kFull, in_list && (e.meta & 1u));
+    if (lane == 0) G.newmask[i] = nm;
+    if (static_cast<int>(lane) == k - 1) G.kth[i] = e.key;
+}
+
+// Alg. 3 line 11: G[i] = k smallest unique keys of the refined list
+// and the reserved half G^v.
+__global__ void k_ggm_finalize(Dims D, Graph G, const uint64_t* __restrict__ reserved) {
+    extern __shared__ Elem fin_scratch[];
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (i >= D.n) return;
+    const uint32_t lane = lane_id();
+    const int k = D.k, kr = k - (k + 1) / 2;
+    Elem cur{static_cast<int>(lane) < k ? G.keys[static_cast<size_t>(i) * k + lane] : kSentinel, 0u};
+    const uint64_t cand = static_cast<int>(lane) < kr ? reserved[static_cast<size_t>(i) * kr + lane] : kSentinel;
+    warp_merge_chunk(cur, cand, fin_scratch + (threadIdx.x >> 5) * 32);
+    if (static_cast<int>(lane) < k) G.keys[static_cast<size_t>(i) * k + lane] = cur.key;
+}
+
+}  // namespace knng

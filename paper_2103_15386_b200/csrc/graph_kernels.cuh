@@ -1,0 +1,400 @@
+// graph_kernels.cuh -- init, list update + sampling, reverse sampling (CSR),
+// state export.  Warp-per-node kernels: one k-NN list (k <= 32 entries) is
+// one u64 key per lane, so every list operation is a register/shuffle
+// operation and every list read/write is one coalesced 256-B transaction.
+#pragma once
+#include "common.cuh"
+
+namespace knng {
+
+struct DevStats {  // device mirror of knng_iter_stats
+    unsigned long long joins, sum_m, sum_q, dist_evals, candidates, appended, overflow, rows;
+};
+
+struct Graph {
+    uint64_t* keys;     // [n][k] ascending
+    uint32_t* newmask;  // [n]    bit j = entry j is NEW
+    uint64_t* kth;      // [n]    k-th key at iteration start (update threshold)
+    uint32_t* lock;     // [n]    spinlock of the overflow insert path
+    uint32_t* bcnt;     // [n]    candidates appended to the bucket
+    uint64_t* bucket;   // [n][B] candidate keys of the current iteration
+};
+
+struct Samples {
+    uint32_t* fwd;   // [2][n][p]   forward NEW / OLD samples
+    uint8_t* fcnt;   // [n][2]
+    uint32_t* rcnt;  // [2][n]      reverse counts, then cursors
+    uint32_t* roff;  // [2][n+1]    reverse CSR offsets
+    uint32_t* rsrc;  // [2][n*p]    reverse sources
+    uint32_t* G;     // [2][n][cap] G_new / G_old, sorted unique
+    uint8_t* gcnt;   // [n][2]      m = |G_new|, q = |G_old|
+    uint32_t* bsum;  // [2][nblk]   scan block sums
+};
+
+struct Dims {
+    int64_t n;
+    int d, k, p, cap, B;
+};
+
+__device__ __forceinline__ uint32_t kmask_of(int k) { return k >= 32 ? kFull : ((1u << k) - 1u); }
+
+// ------------------------------------------------------------------ init
+// Alg. 1 lines 1-4: k distinct random ids != s (D1, D2) drawn in
+// counter order j = 0, 1, ... from Philox(INIT, s, j, s >> 32), canonical
+// distances, sorted by key (D3), all NEW.
+template <typename T, bool COS>
+__global__ void k_init(const T* __restrict__ X, const float* __restrict__ Xn, Dims D,
+                       uint64_t seed, Graph G) {
+    const int64_t s = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (s >= D.n) return;
+    const uint32_t lane = lane_id();
+    const int k = D.k;
+    const uint2 key = seed_key(seed);
+    uint32_t chosen = 0xFFFFFFFFu;
+    int cnt = 0;
+    for (uint32_t j0 = 0; cnt < k; j0 += 32) {
+        const uint4 o = philox4x32_10(
+            make_uint4(kTagInit, static_cast<uint32_t>(s), j0 + lane, static_cast<uint32_t>(static_cast<uint64_t>(s) >> 32)),
+            key);
+        const uint64_t r = uniform_below(o, static_cast<uint64_t>(D.n - 1));
+        const uint32_t v = static_cast<uint32_t>(r + (r >= static_cast<uint64_t>(s) ? 1 : 0));
+        bool dup = false;
+        for (int t = 0; t < cnt; ++t) dup |= (__shfl_sync(kFull, chosen, t) == v);
+        for (int l = 0; l < 32; ++l) {
+            const uint32_t vl = __shfl_sync(kFull, v, l);
+            dup |= (static_cast<uint32_t>(l) < lane && vl == v);
+        }
+        const uint32_t acc = __ballot_sync(kFull, !dup);
+        const int want = static_cast<int>(lane) - cnt;
+        const bool take = want >= 0 && want < __popc(acc) && static_cast<int>(lane) < k;
+        const int src = take ? static_cast<int>(__fns(acc, 0, want + 1)) : 0;
+        const uint32_t got = __shfl_sync(kFull, v, src);
+        if (take) chosen = got;
+        cnt = min(k, cnt + __popc(acc));
+    }
+    uint64_t kk = kSentinel;
+    if (static_cast<int>(lane) < k) {
+        float dist;
+        if constexpr (COS) {
+            dist = Canon<float>::cos(Xn + static_cast<size_t>(s) * D.d, Xn + static_cast<size_t>(chosen) * D.d, D.d);
+        } else {
+            dist = Canon<T>::l2(X + static_cast<size_t>(s) * D.d, X + static_cast<size_t>(chosen) * D.d, D.d);
+        }
+        kk = make_key(dist, chosen);
+    }
+    kk = warp_sort_u64(kk);
+    if (static_cast<int>(lane) < k) G.keys[static_cast<size_t>(s) * k + lane] = kk;
+    if (lane == 0) G.newmask[s] = kmask_of(k);
+    if (static_cast<int>(lane) == k - 1) G.kth[s] = kk;
+}
+
+// ---------------------------------------------------- list update + sample
+// One warp per node s.
+//  do_merge : G'[s] = k smallest unique of G[s] U bucket[s] (D16-D17);
+//             survivors keep their flag, newcomers are NEW.
+//  do_sample: forward samples FN(s) = first min(p, #NEW) NEW entries and
+//             FO(s) = first min(p, #OLD) OLD entries in list order (P:147,
+//             D7); FN entries are marked OLD (D12-D13); reverse counts
+//             for the CSR of P:149.
+__global__ void k_merge_sample(Dims D, Graph G, Samples S, int do_merge, int do_sample) {
+    extern __shared__ Elem smem_scratch[];
+    const int64_t s = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (s >= D.n) return;
+    Elem* scratch = smem_scratch + (threadIdx.x >> 5) * 32;
+    const uint32_t lane = lane_id();
+    const int k = D.k, p = D.p;
+    const bool in_list = static_cast<int>(lane) < k;
+    const uint32_t mask = G.newmask[s];
+    Elem cur{in_list ? G.keys[static_cast<size_t>(s) * k + lane] : kSentinel,
+             in_list ? ((mask >> lane) & 1u) : 0u};
+    bool changed = false;
+    if (do_merge) {
+        const uint32_t c = min(G.bcnt[s], static_cast<uint32_t>(D.B));
+        for (uint32_t base = 0; base < c; base += 32) {
+            const uint64_t cand = (base + lane < c) ? G.bucket[static_cast<size_t>(s) * D.B + base + lane] : kSentinel;
+            warp_merge_chunk(cur, cand, scratch);
+        }
+        if (c > 0) {
+            changed = true;
+            if (!in_list) cur = Elem{kSentinel, 0u};
+        }
+        if (lane == 0) G.bcnt[s] = 0;
+    }
+    if (do_sample) {
+        const bool isnew = in_list && (cur.meta & 1u);
+        const bool isold = in_list && !(cur.meta & 1u);
+        const uint32_t newb = __ballot_sync(kFull, isnew);
+        const uint32_t oldb = __ballot_sync(kFull, isold);
+        const int rn = __popc(newb & lanemask_lt());
+        const int ro = __popc(oldb & lanemask_lt());
+        const uint32_t id = key_id(cur.key);
+        if (isnew && rn < p) {
+            S.fwd[static_cast<size_t>(s) * p + rn] = id;
+            atomicAdd(S.rcnt + id, 1u);
+            cur.meta &= ~1u;  // "Mark all sampled neighbors as OLD"
+        }
+        if (isold && ro < p) {
+            S.fwd[static_cast<size_t>(D.n) * p + static_cast<size_t>(s) * p + ro] = id;
+            atomicAdd(S.rcnt + D.n + id, 1u);
+        }
+        if (lane == 0) {
+            S.fcnt[2 * s] = static_cast<uint8_t>(min(__popc(newb), p));
+            S.fcnt[2 * s + 1] = static_cast<uint8_t>(min(__popc(oldb), p));
+        }
+    }
+    if (changed && in_list) G.keys[static_cast<size_t>(s) * k + lane] = cur.key;
+    const uint32_t nm = __ballot_sync(kFull, in_list && (cur.meta & 1u));
+    if (lane == 0) G.newmask[s] = nm;
+    if (static_cast<int>(lane) == k - 1) G.kth[s] = cur.key;
+}
+
+// ------------------------------------------------- reverse CSR
+// Exclusive scan of rcnt[2][n] into roff[2][n+1]; the counts are zeroed so
+// they serve as scatter cursors.  Three phases, 1024 items per block.
+constexpr int kScanBlock = 1024;
+
+__device__ __forceinline__ uint32_t block_inclusive_scan(uint32_t v, uint32_t* warp_tot) {
+    const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(kFull, v, o);
+        if (lane >= static_cast<uint32_t>(o)) v += t;
+    }
+    if (lane == 31) warp_tot[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t x = lane < (blockDim.x >> 5) ? warp_tot[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(kFull, x, o);
+            if (lane >= static_cast<uint32_t>(o)) x += t;
+        }
+        warp_tot[lane] = x;
+    }
+    __syncthreads();
+    if (w > 0) v += warp_tot[w - 1];
+    return v;
+}
+
+__global__ void k_scan_reduce(const uint32_t* __restrict__ cnt, int64_t n, uint32_t* bsum, int64_t nblk) {
+    __shared__ uint32_t wt[32];
+    const int f = blockIdx.y;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * kScanBlock + threadIdx.x;
+    uint32_t v = i < n ? cnt[f * n + i] : 0u;
+    v = block_inclusive_scan(v, wt);
+    if (threadIdx.x == kScanBlock - 1) bsum[f * nblk + blockIdx.x] = v;
+}
+
+__global__ void k_scan_bsums(uint32_t* bsum, int64_t nblk) {
+    __shared__ uint32_t wt[32];
+    const int f = blockIdx.x;
+    uint32_t* b = bsum + f * nblk;
+    const int64_t per = (nblk + kScanBlock - 1) / kScanBlock;
+    const int64_t lo = threadIdx.x * per, hi = min(nblk, lo + per);
+    uint32_t sum = 0;
+    for (int64_t i = lo; i < hi; ++i) sum += b[i];
+    const uint32_t incl = block_inclusive_scan(sum, wt);
+    uint32_t run = incl - sum;
+    for (int64_t i = lo; i < hi; ++i) {
+        const uint32_t x = b[i];
+        b[i] = run;
+        run += x;
+    }
+}
+
+__global__ void k_scan_final(uint32_t* cnt, int64_t n, const uint32_t* __restrict__ bsum, int64_t nblk,
+                             uint32_t* off) {
+    __shared__ uint32_t wt[32];
+    const int f = blockIdx.y;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * kScanBlock + threadIdx.x;
+    const uint32_t v = i < n ? cnt[f * n + i] : 0u;
+    const uint32_t incl = block_inclusive_scan(v, wt) + bsum[f * nblk + blockIdx.x];
+    if (i < n) {
+        off[f * (n + 1) + i] = incl - v;
+        cnt[f * n + i] = 0u;
+        if (i == n - 1) off[f * (n + 1) + n] = incl;
+    }
+}
+
+// reverse append of P:149 as a CSR scatter: s goes to the list of every v in
+// its forward samples.  Order inside a list is arbitrary; the selection that
+// follows is order-independent (D10).
+__global__ void k_rev_scatter(Dims D, Samples S) {
+    const int f = blockIdx.y;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= D.n * D.p) return;
+    const int64_t s = i / D.p;
+    const int j = static_cast<int>(i - s * D.p);
+    if (j >= S.fcnt[2 * s + f]) return;
+    const uint32_t v = S.fwd[static_cast<size_t>(f) * D.n * D.p + i];
+    const uint32_t pos = atomicAdd(S.rcnt + f * D.n + v, 1u);
+    S.rsrc[static_cast<size_t>(f) * D.n * D.p + S.roff[f * (D.n + 1) + v] + pos] = static_cast<uint32_t>(s);
+}
+
+__device__ __forceinline__ uint64_t warp_bitonic_merge_u64(uint64_t x) {
+    const uint32_t lane = lane_id();
+#pragma unroll
+    for (int j = 16; j > 0; j >>= 1) {
+        const uint64_t o = shfl_xor_u64(x, j);
+        const bool lower = (lane & j) == 0;
+        x = lower ? (o < x ? o : x) : (o < x ? x : o);
+    }
+    return x;
+}
+
+// sort + dedup one u32 id per lane (0xFFFFFFFF = empty); returns the unique
+// sorted ids compacted to lanes [0, count) and sets count.
+__device__ __forceinline__ uint32_t warp_sort_unique_ids(uint32_t id, int& count) {
+    const uint32_t lane = lane_id();
+    uint64_t x = id == 0xFFFFFFFFu ? kSentinel : static_cast<uint64_t>(id);
+    x = warp_sort_u64(x);
+    const uint64_t prev = shfl_u64(x, (lane + 31) & 31);
+    const bool ok = x != kSentinel && (lane == 0 || x != prev);
+    const uint32_t okm = __ballot_sync(kFull, ok);
+    count = __popc(okm);
+    const int src = static_cast<int>(lane) < count ? static_cast<int>(__fns(okm, 0, lane + 1)) : 0;
+    const uint64_t got = shfl_u64(x, src);
+    return static_cast<int>(lane) < count ? static_cast<uint32_t>(got) : 0xFFFFFFFFu;
+}
+
+// One warp per node v: G(v) = sort_unique(F(v) U c smallest-priority reverse
+// sources), c = 2p - |F(v)| (P:149 cap 2p with the forward samples counted,
+// D8; priority key (Philox(tag, tword, s, v).x, s), D10; P:151 dedup), then
+// G_old(v) minus G_new(v) (D11).  Requires 2p <= 32.
+__global__ void k_rev_select(Dims D, Samples S, uint32_t tword, uint64_t seed) {
+    const int64_t v = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (v >= D.n) return;
+    const uint32_t lane = lane_id();
+    const uint2 key = seed_key(seed);
+    const int p = D.p, cap = D.cap;
+    uint32_t gnew = 0xFFFFFFFFu;
+    int m = 0;
+    for (int f = 0; f < 2; ++f) {
+        const int fc = S.fcnt[2 * v + f];
+        const uint32_t* fwd = S.fwd + static_cast<size_t>(f) * D.n * p + static_cast<size_t>(v) * p;
+        const uint32_t* rs = S.rsrc + static_cast<size_t>(f) * D.n * p;
+        const uint32_t o0 = S.roff[f * (D.n + 1) + v], o1 = S.roff[f * (D.n + 1) + v + 1];
+        const int r = static_cast<int>(o1 - o0);
+        const int c = cap - fc;
+        uint32_t e = 0xFFFFFFFFu;
+        if (static_cast<int>(lane) < fc) e = fwd[lane];
+        if (r <= c) {
+            const int j = static_cast<int>(lane) - fc;
+            if (j >= 0 && j < r) e = rs[o0 + j];
+        } else {
+            uint64_t best = kSentinel;  // running 32 smallest (prio, s), sorted
+            for (int base = 0; base < r; base += 32) {
+                uint64_t x = kSentinel;
+                if (base + static_cast<int>(lane) < r) {
+                    const uint32_t src = rs[o0 + base + lane];
+                    const uint4 o = philox4x32_10(
+                        make_uint4(f == 0 ? kTagRevNew : kTagRevOld, tword, src, static_cast<uint32_t>(v)), key);
+                    x = (static_cast<uint64_t>(o.x) << 32) | src;
+                }
+                x = warp_sort_u64(x);
+                const uint64_t xr = shfl_u64(x, 31 - lane);
+                best = warp_bitonic_merge_u64(xr < best ? xr : best);
+            }
+            const int j = static_cast<int>(lane) - fc;
+            const uint64_t got = shfl_u64(best, j >= 0 && j < c ? j : 0);
+            if (j >= 0 && j < c) e = static_cast<uint32_t>(got);
+        }
+        int cnt = 0;
+        uint32_t u = warp_sort_unique_ids(e, cnt);
+        if (f == 0) {
+            gnew = u;
+            m = cnt;
+        } else {
+            // D11: drop ids that are also NEW samples
+            bool in_new = false;
+            for (int t = 0; t < m; ++t) in_new |= (__shfl_sync(kFull, gnew, t) == u);
+            const bool keep = static_cast<int>(lane) < cnt && !in_new;
+            const uint32_t km = __ballot_sync(kFull, keep);
+            cnt = __popc(km);
+            const int src = static_cast<int>(lane) < cnt ? static_cast<int>(__fns(km, 0, lane + 1)) : 0;
+            u = __shfl_sync(kFull, u, src);
+        }
+        if (static_cast<int>(lane) < cnt) S.G[static_cast<size_t>(f) * D.n * cap + static_cast<size_t>(v) * cap + lane] = u;
+        if (lane == 0) {
+            S.gcnt[2 * v + f] = static_cast<uint8_t>(cnt);
+            S.rcnt[f * D.n + v] = 0u;  // cursors back to zero for the next iteration
+        }
+    }
+}
+
+// ------------------------------------------------------------------ export
+__global__ void k_export(const uint64_t* __restrict__ keys, int64_t total, uint32_t* ids, float* dists) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    const uint64_t kk = keys[i];
+    if (ids) ids[i] = key_id(kk);
+    if (dists) dists[i] = key_dist(kk);
+}
+
+// debug-ABI state conversions: flags u8 [n][k] <-> newmask, plus kth
+__global__ void k_state_in(Dims D, Graph G, const uint8_t* __restrict__ flags) {
+    const int64_t s = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (s >= D.n) return;
+    const uint32_t lane = lane_id();
+    const bool in_list = static_cast<int>(lane) < D.k;
+    const bool f = in_list && flags[static_cast<size_t>(s) * D.k + lane] != 0;
+    const uint32_t nm = __ballot_sync(kFull, f);
+    if (lane == 0) {
+        G.newmask[s] = nm;
+        G.bcnt[s] = 0;
+        G.lock[s] = 0;
+        G.kth[s] = G.keys[static_cast<size_t>(s) * D.k + D.k - 1];
+    }
+}
+
+__global__ void k_state_out(Dims D, Graph G, uint8_t* flags) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= D.n * D.k) return;
+    const int64_t s = i / D.k;
+    const int j = static_cast<int>(i - s * D.k);
+    flags[i] = static_cast<uint8_t>((G.newmask[s] >> j) & 1u);
+}
+
+// Debug copy of G_new/G_old tables into [n][cap] + int32 counts
+__global__ void k_samples_out(Dims D, Samples S, uint32_t* Gn, int32_t* cn, uint32_t* Go, int32_t* co) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= D.n * D.cap) return;
+    const int64_t v = i / D.cap;
+    const int j = static_cast<int>(i - v * D.cap);
+    const int m = S.gcnt[2 * v], q = S.gcnt[2 * v + 1];
+    Gn[i] = j < m ? S.G[i] : 0u;
+    Go[i] = j < q ? S.G[static_cast<size_t>(D.n) * D.cap + i] : 0u;
+    if (j == 0) {
+        cn[v] = m;
+        co[v] = q;
+    }
+}
+
+// cosine: x^ = x * (1 / sqrtf(sum fmaf(x_i, x_i))) (D6); flags a zero row
+__global__ void k_normalize(const float* __restrict__ X, int64_t n, int d, float* Xn, int* bad) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float* x = X + static_cast<size_t>(i) * d;
+    float acc = 0.0f;
+    for (int j = 0; j < d; ++j) acc = fmaf(x[j], x[j], acc);
+    if (!(acc > 0.0f)) {
+        atomicExch(bad, 1);
+        return;
+    }
+    const float r = 1.0f / sqrtf(acc);
+    float* y = Xn + static_cast<size_t>(i) * d;
+    for (int j = 0; j < d; ++j) y[j] = x[j] * r;
+}
+
+__global__ void k_philox_test(const uint32_t* __restrict__ ctr, int64_t m, uint64_t seed, uint32_t* out) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const uint4 c = make_uint4(ctr[4 * i], ctr[4 * i + 1], ctr[4 * i + 2], ctr[4 * i + 3]);
+    const uint4 o = philox4x32_10(c, seed_key(seed));
+    out[4 * i] = o.x;
+    out[4 * i + 1] = o.y;
+    out[4 * i + 2] = o.z;
+    out[4 * i + 3] = o.w;
+}
+
+}  // namespace knng

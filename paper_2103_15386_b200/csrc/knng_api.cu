@@ -1,0 +1,728 @@
+// knng_api.cu -- the C ABI of include/knng.h: validation, workspace layout,
+// stream-ordered orchestration of the kernels, error mapping, counters.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/knng.h"
+#include "eval_kernels.cuh"
+#include "ggm_kernels.cuh"
+#include "join_kernel.cuh"
+
+using namespace knng;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local std::vector<knng_iter_stats> g_last_stats;
+std::atomic<int64_t> g_launches{0};
+std::atomic<int> g_timing{0};
+std::mutex g_time_mu;
+std::map<std::string, std::pair<double, int64_t>> g_times;
+
+knng_status fail(knng_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+constexpr int kMaxIters = 256;
+
+// ---------------------------------------------------------------- layout
+struct Layout {
+    size_t keys, newmask, kth, lock, bcnt, bucket, fwd, fcnt, rcnt, roff, rsrc, G, gcnt, bsum, stats,
+        xnorm, reserved, flag, total;
+};
+
+int bucket_cap(int k) { return k <= 16 ? 32 : 64; }
+int64_t scan_blocks(int64_t n) { return (n + kScanBlock - 1) / kScanBlock; }
+
+size_t align_up(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+
+Layout make_layout(int64_t n, int d, int k, int p, bool cosine, bool own_keys, bool merge) {
+    Layout L{};
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t at = off;
+        off += align_up(bytes);
+        return at;
+    };
+    const int cap = 2 * p, B = bucket_cap(k);
+    L.keys = own_keys ? take(static_cast<size_t>(n) * k * 8) : 0;
+    L.newmask = take(static_cast<size_t>(n) * 4);
+    L.kth = take(static_cast<size_t>(n) * 8);
+    L.lock = take(static_cast<size_t>(n) * 4);
+    L.bcnt = take(static_cast<size_t>(n) * 4);
+    L.bucket = take(static_cast<size_t>(n) * B * 8);
+    L.fwd = take(static_cast<size_t>(2) * n * p * 4);
+    L.fcnt = take(static_cast<size_t>(n) * 2);
+    L.rcnt = take(static_cast<size_t>(2) * n * 4);
+    L.roff = take(static_cast<size_t>(2) * (n + 1) * 4);
+    L.rsrc = take(static_cast<size_t>(2) * n * p * 4);
+    L.G = take(static_cast<size_t>(2) * n * cap * 4);
+    L.gcnt = take(static_cast<size_t>(n) * 2);
+    L.bsum = take(static_cast<size_t>(2) * scan_blocks(n) * 4);
+    L.stats = take(sizeof(DevStats) * kMaxIters);
+    L.xnorm = cosine ? take(static_cast<size_t>(n) * d * 4) : 0;
+    L.reserved = merge ? take(static_cast<size_t>(n) * (k / 2 > 0 ? k / 2 : 1) * 8) : 0;
+    L.flag = take(16);
+    L.total = off;
+    return L;
+}
+
+// ---------------------------------------------------------------- context
+struct Ctx {
+    cudaStream_t stream = nullptr;
+    bool timing = false;
+    std::vector<cudaEvent_t> pool;
+    std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
+    void* owned_ws = nullptr;
+    cudaError_t err = cudaSuccess;
+    std::string err_where;
+
+    cudaEvent_t ev() {
+        cudaEvent_t e = nullptr;
+        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+        pool.push_back(e);
+        return e;
+    }
+    ~Ctx() {
+        for (auto e : pool) cudaEventDestroy(e);
+        if (owned_ws) cudaFreeAsync(owned_ws, stream);
+    }
+    // launch bookkeeping: count, optional events, error capture
+    template <typename F>
+    bool launch(const char* name, F&& f) {
+        if (err != cudaSuccess) return false;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (timing) {
+            e0 = ev();
+            if (e0) cudaEventRecord(e0, stream);
+        }
+        f();
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        if (timing) {
+            e1 = ev();
+            if (e1) cudaEventRecord(e1, stream);
+            if (e0 && e1) marks.push_back({name, {e0, e1}});
+        }
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) {
+            err = e;
+            err_where = name;
+            return false;
+        }
+        return true;
+    }
+    knng_status finish() {
+        const cudaError_t se = cudaStreamSynchronize(stream);
+        if (err == cudaSuccess && se != cudaSuccess) {
+            err = se;
+            err_where = "stream synchronize";
+        }
+        if (err != cudaSuccess)
+            return fail(KNNG_E_CUDA, "CUDA error in %s: %s", err_where.c_str(), cudaGetErrorString(err));
+        if (timing) {
+            std::lock_guard<std::mutex> lk(g_time_mu);
+            for (auto& m : marks) {
+                float ms = 0.f;
+                if (cudaEventElapsedTime(&ms, m.second.first, m.second.second) == cudaSuccess) {
+                    auto& t = g_times[m.first];
+                    t.first += ms;
+                    t.second += 1;
+                }
+            }
+        }
+        return KNNG_OK;
+    }
+};
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+knng_status check_common(knng_dtype dt, int64_t n, int32_t d, int32_t k, knng_metric metric, int32_t p) {
+    if (dt != KNNG_F32 && dt != KNNG_U8) return fail(KNNG_E_USAGE, "unknown dtype %d", static_cast<int>(dt));
+    if (metric != KNNG_L2SQ && metric != KNNG_COSINE) return fail(KNNG_E_USAGE, "unknown metric %d", static_cast<int>(metric));
+    if (metric == KNNG_COSINE && dt != KNNG_F32) return fail(KNNG_E_USAGE, "cosine requires float32 vectors");
+    if (d < 1) return fail(KNNG_E_USAGE, "d must be >= 1 (got %d)", d);
+    if (k < 2 || k > 32) return fail(KNNG_E_USAGE, "k must be in [2, 32] (got %d)", k);
+    if (p < 1 || p >= k) return fail(KNNG_E_USAGE, "sample_size must satisfy 1 <= p < k (got p=%d, k=%d)", p, k);
+    if (2 * p > 32) return fail(KNNG_E_USAGE, "sample_size must be <= 16 in this version (got %d)", p);
+    if (n <= k) return fail(KNNG_E_USAGE, "n must exceed k (n=%lld, k=%d)", static_cast<long long>(n), k);
+    if (n >= 0xFFFFFFFFll) return fail(KNNG_E_USAGE, "n must be < 2^32 - 1");
+    if (n * static_cast<int64_t>(p) >= (1ll << 32)) return fail(KNNG_E_USAGE, "n * sample_size must be < 2^32");
+    return KNNG_OK;
+}
+
+struct Run {
+    Ctx& c;
+    Layout L;
+    char* ws;
+    Dims D;
+    Graph G;
+    Samples S;
+    DevStats* stats;
+    const void* X;
+    knng_dtype dt;
+    knng_metric metric;
+    const float* Xn;
+    uint64_t seed;
+    int64_t boundary = -1;
+
+    Run(Ctx& ctx) : c(ctx) {}
+
+    void bind(char* base, uint64_t* keys) {
+        ws = base;
+        G.keys = keys ? keys : reinterpret_cast<uint64_t*>(ws + L.keys);
+        G.newmask = reinterpret_cast<uint32_t*>(ws + L.newmask);
+        G.kth = reinterpret_cast<uint64_t*>(ws + L.kth);
+        G.lock = reinterpret_cast<uint32_t*>(ws + L.lock);
+        G.bcnt = reinterpret_cast<uint32_t*>(ws + L.bcnt);
+        G.bucket = reinterpret_cast<uint64_t*>(ws + L.bucket);
+        S.fwd = reinterpret_cast<uint32_t*>(ws + L.fwd);
+        S.fcnt = reinterpret_cast<uint8_t*>(ws + L.fcnt);
+        S.rcnt = reinterpret_cast<uint32_t*>(ws + L.rcnt);
+        S.roff = reinterpret_cast<uint32_t*>(ws + L.roff);
+        S.rsrc = reinterpret_cast<uint32_t*>(ws + L.rsrc);
+        S.G = reinterpret_cast<uint32_t*>(ws + L.G);
+        S.gcnt = reinterpret_cast<uint8_t*>(ws + L.gcnt);
+        S.bsum = reinterpret_cast<uint32_t*>(ws + L.bsum);
+        stats = reinterpret_cast<DevStats*>(ws + L.stats);
+        Xn = metric == KNNG_COSINE ? reinterpret_cast<const float*>(ws + L.xnorm) : nullptr;
+    }
+
+    int warps_grid(int64_t items, int warps_per_block) const {
+        return static_cast<int>((items + warps_per_block - 1) / warps_per_block);
+    }
+
+    bool zero_state() {
+        if (c.err != cudaSuccess) return false;
+        cudaMemsetAsync(G.lock, 0, static_cast<size_t>(D.n) * 4, c.stream);
+        cudaMemsetAsync(G.bcnt, 0, static_cast<size_t>(D.n) * 4, c.stream);
+        cudaMemsetAsync(S.rcnt, 0, static_cast<size_t>(2) * D.n * 4, c.stream);
+        cudaMemsetAsync(stats, 0, sizeof(DevStats) * kMaxIters, c.stream);
+        return true;
+    }
+
+    // cosine: normalised copy of the rows (D6); KNNG_E_DOMAIN on a zero row
+    knng_status normalize() {
+        if (metric != KNNG_COSINE) return KNNG_OK;
+        int* flag = reinterpret_cast<int*>(ws + L.flag);
+        cudaMemsetAsync(flag, 0, 4, c.stream);
+        c.launch("k_normalize", [&] {
+            k_normalize<<<static_cast<int>((D.n + 255) / 256), 256, 0, c.stream>>>(
+                static_cast<const float*>(X), D.n, D.d, const_cast<float*>(Xn), flag);
+        });
+        int h = 0;
+        cudaMemcpyAsync(&h, flag, 4, cudaMemcpyDeviceToHost, c.stream);
+        const cudaError_t e = cudaStreamSynchronize(c.stream);
+        if (c.err == cudaSuccess && e != cudaSuccess) {
+            c.err = e;
+            c.err_where = "normalize";
+        }
+        if (c.err != cudaSuccess) return KNNG_OK;  // reported by finish()
+        if (h) return fail(KNNG_E_DOMAIN, "zero vector under the cosine metric");
+        return KNNG_OK;
+    }
+
+    void init() {
+        const int wpb = 8;
+        const int grid = warps_grid(D.n, wpb);
+        c.launch("k_init", [&] {
+            if (metric == KNNG_COSINE)
+                k_init<float, true><<<grid, wpb * 32, 0, c.stream>>>(nullptr, Xn, D, seed, G);
+            else if (dt == KNNG_F32)
+                k_init<float, false><<<grid, wpb * 32, 0, c.stream>>>(static_cast<const float*>(X), nullptr, D, seed, G);
+            else
+                k_init<uint8_t, false><<<grid, wpb * 32, 0, c.stream>>>(static_cast<const uint8_t*>(X), nullptr, D, seed, G);
+        });
+    }
+
+    void merge_sample(int do_merge, int do_sample) {
+        const int wpb = 8;
+        const int grid = warps_grid(D.n, wpb);
+        c.launch(do_sample ? "k_merge_sample" : "k_merge", [&] {
+            k_merge_sample<<<grid, wpb * 32, wpb * 32 * sizeof(Elem), c.stream>>>(D, G, S, do_merge, do_sample);
+        });
+    }
+
+    void reverse(uint32_t tword) {
+        const int64_t nb = scan_blocks(D.n);
+        c.launch("k_scan_reduce", [&] {
+            k_scan_reduce<<<dim3(static_cast<unsigned>(nb), 2), kScanBlock, 0, c.stream>>>(S.rcnt, D.n, S.bsum, nb);
+        });
+        c.launch("k_scan_bsums", [&] { k_scan_bsums<<<2, kScanBlock, 0, c.stream>>>(S.bsum, nb); });
+        c.launch("k_scan_final", [&] {
+            k_scan_final<<<dim3(static_cast<unsigned>(nb), 2), kScanBlock, 0, c.stream>>>(S.rcnt, D.n, S.bsum, nb, S.roff);
+        });
+        const int64_t items = D.n * D.p;
+        c.launch("k_rev_scatter", [&] {
+            k_rev_scatter<<<dim3(static_cast<unsigned>((items + 255) / 256), 2), 256, 0, c.stream>>>(D, S);
+        });
+        const int wpb = 8;
+        c.launch("k_rev_select", [&] {
+            k_rev_select<<<warps_grid(D.n, wpb), wpb * 32, 0, c.stream>>>(D, S, tword, seed);
+        });
+    }
+
+    void join(int iter) {
+        const int grid = static_cast<int>(D.n < (1 << 20) ? D.n : (1 << 20));
+        DevStats* st = stats + iter;
+        const size_t esz = (metric == KNNG_COSINE || dt == KNNG_F32) ? 4 : 1;
+        const uintptr_t base = metric == KNNG_COSINE ? reinterpret_cast<uintptr_t>(Xn) : reinterpret_cast<uintptr_t>(X);
+        const int al = ((static_cast<size_t>(D.d) * esz) % 16 == 0 && base % 16 == 0) ? 1 : 0;
+        c.launch("k_join", [&] {
+            if (metric == KNNG_COSINE)
+                k_join<float, true><<<grid, kJoinThreads, 0, c.stream>>>(nullptr, Xn, D, G, S, boundary, al, st);
+            else if (dt == KNNG_F32)
+                k_join<float, false><<<grid, kJoinThreads, 0, c.stream>>>(static_cast<const float*>(X), nullptr, D, G, S, boundary, al, st);
+            else
+                k_join<uint8_t, false><<<grid, kJoinThreads, 0, c.stream>>>(static_cast<const uint8_t*>(X), nullptr, D, G, S, boundary, al, st);
+        });
+    }
+
+    void iteration(int iter, uint32_t tword, bool merge_first) {
+        merge_sample(merge_first ? 1 : 0, 1);
+        reverse(tword);
+        join(iter);
+    }
+
+    void export_graph(uint32_t* ids, float* dists) {
+        const int64_t total = D.n * D.k;
+        c.launch("k_export", [&] {
+            k_export<<<static_cast<int>((total + 255) / 256), 256, 0, c.stream>>>(G.keys, total, ids, dists);
+        });
+    }
+
+    void collect_stats(int iters) {
+        std::vector<DevStats> h(iters > 0 ? iters : 1);
+        if (c.err == cudaSuccess && iters > 0) {
+            cudaMemcpyAsync(h.data(), stats, sizeof(DevStats) * iters, cudaMemcpyDeviceToHost, c.stream);
+            cudaStreamSynchronize(c.stream);
+        }
+        g_last_stats.clear();
+        for (int i = 0; i < iters; ++i) {
+            knng_iter_stats s;
+            s.joins = static_cast<int64_t>(h[i].joins);
+            s.sum_m = static_cast<int64_t>(h[i].sum_m);
+            s.sum_q = static_cast<int64_t>(h[i].sum_q);
+            s.dist_evals = static_cast<int64_t>(h[i].dist_evals);
+            s.candidates = static_cast<int64_t>(h[i].candidates);
+            s.appended = static_cast<int64_t>(h[i].appended);
+            s.overflow = static_cast<int64_t>(h[i].overflow);
+            s.rows = static_cast<int64_t>(h[i].rows);
+            g_last_stats.push_back(s);
+        }
+    }
+};
+
+knng_status get_workspace(Ctx& c, void* workspace, size_t bytes, size_t need, char** out) {
+    if (workspace == nullptr && bytes == 0) {
+        void* p = nullptr;
+        const cudaError_t e = cudaMallocAsync(&p, need, c.stream);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(KNNG_E_NOMEM, "cannot allocate %zu bytes of workspace: %s", need, cudaGetErrorString(e));
+        }
+        c.owned_ws = p;
+        *out = static_cast<char*>(p);
+        return KNNG_OK;
+    }
+    if (bytes < need) return fail(KNNG_E_USAGE, "workspace too small: %zu < %zu bytes", bytes, need);
+    if (!is_device_ptr(workspace)) return fail(KNNG_E_USAGE, "workspace is not a device pointer");
+    *out = static_cast<char*>(workspace);
+    return KNNG_OK;
+}
+
+}  // namespace
+
+// ======================================================================
+extern "C" {
+
+size_t knng_build_workspace_bytes(knng_dtype dt, int64_t n, int32_t d, int32_t k, int32_t sample_size,
+                                  knng_metric metric) {
+    if (check_common(dt, n, d, k, metric, sample_size) != KNNG_OK) return 0;
+    return make_layout(n, d, k, sample_size, metric == KNNG_COSINE, true, false).total;
+}
+
+knng_status knng_build(const void* vectors, knng_dtype dt, int64_t n, int32_t d, int32_t k, knng_metric metric,
+                       int32_t iters, int32_t sample_size, uint64_t seed, uint32_t* out_ids, float* out_dists,
+                       void* workspace, size_t workspace_bytes, void* stream) {
+    knng_status s = check_common(dt, n, d, k, metric, sample_size);
+    if (s) return s;
+    if (iters < 1 || iters > kMaxIters) return fail(KNNG_E_USAGE, "iters must be in [1, %d] (got %d)", kMaxIters, iters);
+    if (!vectors || !out_ids || !out_dists) return fail(KNNG_E_USAGE, "null pointer argument");
+    if (!is_device_ptr(vectors) || !is_device_ptr(out_ids) || !is_device_ptr(out_dists))
+        return fail(KNNG_E_USAGE, "vectors/out_ids/out_dists must be device pointers");
+    Ctx c;
+    c.stream = static_cast<cudaStream_t>(stream);
+    c.timing = g_timing.load() != 0;
+    Run R(c);
+    R.L = make_layout(n, d, k, sample_size, metric == KNNG_COSINE, true, false);
+    char* ws = nullptr;
+    if ((s = get_workspace(c, workspace, workspace_bytes, R.L.total, &ws))) return s;
+    R.D = Dims{n, d, k, sample_size, 2 * sample_size, bucket_cap(k)};
+    R.X = vectors;
+    R.dt = dt;
+    R.metric = metric;
+    R.seed = seed;
+    R.bind(ws, nullptr);
+    R.zero_state();
+    if ((s = R.normalize())) return s;
+    R.init();
+    for (int t = 0; t < iters; ++t) R.iteration(t, static_cast<uint32_t>(t), t > 0);
+    R.merge_sample(1, 0);
+    R.export_graph(out_ids, out_dists);
+    R.collect_stats(iters);
+    return c.finish();
+}
+
+knng_status knng_build_host(const void* host_vectors, knng_dtype dt, int64_t n, int32_t d, int32_t k,
+                            knng_metric metric, int32_t iters, int32_t sample_size, uint64_t seed,
+                            uint32_t* host_out_ids, float* host_out_dists, void* stream) {
+    knng_status s = check_common(dt, n, d, k, metric, sample_size);
+    if (s) return s;
+    if (iters < 1 || iters > kMaxIters) return fail(KNNG_E_USAGE, "iters must be in [1, %d] (got %d)", kMaxIters, iters);
+    if (!host_vectors || !host_out_ids || !host_out_dists) return fail(KNNG_E_USAGE, "null pointer argument");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t vbytes = static_cast<size_t>(n) * d * (dt == KNNG_F32 ? 4 : 1);
+    const size_t gbytes = static_cast<size_t>(n) * k * 4;
+    void *dv = nullptr, *di = nullptr, *dd = nullptr;
+    cudaError_t e = cudaMallocAsync(&dv, vbytes, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&di, gbytes, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&dd, gbytes, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dv, host_vectors, vbytes, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) {
+        s = knng_build(dv, dt, n, d, k, metric, iters, sample_size, seed, static_cast<uint32_t*>(di),
+                       static_cast<float*>(dd), nullptr, 0, stream);
+        if (s == KNNG_OK) {
+            e = cudaMemcpyAsync(host_out_ids, di, gbytes, cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(host_out_dists, dd, gbytes, cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        }
+    }
+    if (dv) cudaFreeAsync(dv, st);
+    if (di) cudaFreeAsync(di, st);
+    if (dd) cudaFreeAsync(dd, st);
+    cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(e == cudaErrorMemoryAllocation ? KNNG_E_NOMEM : KNNG_E_CUDA, "knng_build_host: %s",
+                    cudaGetErrorString(e));
+    }
+    return s;
+}
+
+knng_status knng_bruteforce(const void* vectors, knng_dtype dt, int64_t n, int32_t d, knng_metric metric,
+                            const int64_t* queries, int64_t nq, int32_t kq, uint32_t* out_ids, float* out_dists,
+                            void* stream) {
+    if (dt != KNNG_F32 && dt != KNNG_U8) return fail(KNNG_E_USAGE, "unknown dtype");
+    if (metric != KNNG_L2SQ && metric != KNNG_COSINE) return fail(KNNG_E_USAGE, "unknown metric");
+    if (metric == KNNG_COSINE && dt != KNNG_F32) return fail(KNNG_E_USAGE, "cosine requires float32 vectors");
+    if (kq < 1 || kq > 32 || n <= kq || d < 1 || nq < 0) return fail(KNNG_E_USAGE, "bad bruteforce arguments");
+    if (nq == 0) return KNNG_OK;
+    if (!is_device_ptr(vectors) || !is_device_ptr(queries) || !is_device_ptr(out_ids) || !is_device_ptr(out_dists))
+        return fail(KNNG_E_USAGE, "bruteforce arguments must be device pointers");
+    Ctx c;
+    c.stream = static_cast<cudaStream_t>(stream);
+    c.timing = g_timing.load() != 0;
+    const bool cosine = metric == KNNG_COSINE;
+    const size_t esz = (cosine || dt == KNNG_F32) ? 4 : 1;
+    const size_t outb = static_cast<size_t>(nq) * kq * 8;
+    const size_t xnb = cosine ? static_cast<size_t>(n) * d * 4 : 0;
+    char* ws = nullptr;
+    knng_status s;
+    if ((s = get_workspace(c, nullptr, 0, align_up(outb) + align_up(xnb) + 256, &ws))) return s;
+    uint64_t* keys = reinterpret_cast<uint64_t*>(ws);
+    float* Xn = cosine ? reinterpret_cast<float*>(ws + align_up(outb)) : nullptr;
+    int* flag = reinterpret_cast<int*>(ws + align_up(outb) + align_up(xnb));
+    if (cosine) {
+        cudaMemsetAsync(flag, 0, 4, c.stream);
+        c.launch("k_normalize", [&] {
+            k_normalize<<<static_cast<int>((n + 255) / 256), 256, 0, c.stream>>>(static_cast<const float*>(vectors), n,
+                                                                                 d, Xn, flag);
+        });
+        int h = 0;
+        cudaMemcpyAsync(&h, flag, 4, cudaMemcpyDeviceToHost, c.stream);
+        cudaStreamSynchronize(c.stream);
+        if (h) return fail(KNNG_E_DOMAIN, "zero vector under the cosine metric");
+    }
+    int W = 8;
+    const int stride = esz == 4 ? bf_stride_elems<float>(d) : bf_stride_elems<uint8_t>(d);
+    auto smem_for = [&](int w) {
+        return static_cast<size_t>(32 + w * kBfQPerWarp) * stride * esz + static_cast<size_t>(w) * 32 * sizeof(Elem);
+    };
+    while (W > 1 && smem_for(W) > 200 * 1024) W >>= 1;
+    const size_t smem = smem_for(W);
+    if (smem > 220 * 1024) return fail(KNNG_E_USAGE, "d too large for the brute-force kernel");
+    const int64_t per_block = static_cast<int64_t>(W) * kBfQPerWarp;
+    const int grid = static_cast<int>((nq + per_block - 1) / per_block);
+    c.launch("k_bruteforce", [&] {
+        if (cosine) {
+            cudaFuncSetAttribute(k_bruteforce<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            k_bruteforce<float, true><<<grid, W * 32, smem, c.stream>>>(nullptr, Xn, n, d, queries, nq, kq, keys);
+        } else if (dt == KNNG_F32) {
+            cudaFuncSetAttribute(k_bruteforce<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            k_bruteforce<float, false><<<grid, W * 32, smem, c.stream>>>(static_cast<const float*>(vectors), nullptr, n, d,
+                                                                          queries, nq, kq, keys);
+        } else {
+            cudaFuncSetAttribute(k_bruteforce<uint8_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            k_bruteforce<uint8_t, false><<<grid, W * 32, smem, c.stream>>>(static_cast<const uint8_t*>(vectors), nullptr, n,
+                                                                            d, queries, nq, kq, keys);
+        }
+    });
+    const int64_t total = nq * kq;
+    c.launch("k_export", [&] {
+        k_export<<<static_cast<int>((total + 255) / 256), 256, 0, c.stream>>>(keys, total, out_ids, out_dists);
+    });
+    return c.finish();
+}
+
+// ------------------------------------------------------------ debug ABI
+knng_status knng_debug_init(const void* vectors, knng_dtype dt, int64_t n, int32_t d, int32_t k,
+                            knng_metric metric, uint64_t seed, uint64_t* keys, uint8_t* flags, void* stream) {
+    knng_status s = check_common(dt, n, d, k, metric, 1);
+    if (s) return s;
+    if (!is_device_ptr(vectors) || !is_device_ptr(keys) || !is_device_ptr(flags))
+        return fail(KNNG_E_USAGE, "arguments must be device pointers");
+    Ctx c;
+    c.stream = static_cast<cudaStream_t>(stream);
+    c.timing = g_timing.load() != 0;
+    Run R(c);
+    R.L = make_layout(n, d, k, 1, metric == KNNG_COSINE, false, false);
+    char* ws = nullptr;
+    if ((s = get_workspace(c, nullptr, 0, R.L.total, &ws))) return s;
+    R.D = Dims{n, d, k, 1, 2, bucket_cap(k)};
+    R.X = vectors;
+    R.dt = dt;
+    R.metric = metric;
+    R.seed = seed;
+    R.bind(ws, keys);
+    if ((s = R.normalize())) return s;
+    R.init();
+    c.launch("k_state_out", [&] {
+        k_state_out<<<static_cast<int>((n * k + 255) / 256), 256, 0, c.stream>>>(R.D, R.G, flags);
+    });
+    return c.finish();
+}
+
+knng_status knng_debug_iterate(const void* vectors, knng_dtype dt, int64_t n, int32_t d, int32_t k,
+                               knng_metric metric, int32_t sample_size, uint32_t tword, uint64_t seed,
+                               int64_t boundary, uint64_t* keys, uint8_t* flags, knng_iter_stats* host_stats,
+                               void* workspace, size_t workspace_bytes, void* stream) {
+    knng_status s = check_common(dt, n, d, k, metric, sample_size);
+    if (s) return s;
+    if (!is_device_ptr(vectors) || !is_device_ptr(keys) || !is_device_ptr(flags))
+        return fail(KNNG_E_USAGE, "arguments must be device pointers");
+    Ctx c;
+    c.stream = static_cast<cudaStream_t>(stream);
+    c.timing = g_timing.load() != 0;
+    Run R(c);
+    R.L = make_layout(n, d, k, sample_size, metric == KNNG_COSINE, false, false);
+    char* ws = nullptr;
+    if ((s = get_workspace(c, workspace, workspace_bytes, R.L.total, &ws))) return s;
+    R.D = Dims{n, d, k, sample_size, 2 * sample_size, bucket_cap(k)};
+    R.X = vectors;
+    R.dt = dt;
+    R.metric = metric;
+    R.seed = seed;
+    R.boundary = boundary;
+    R.bind(ws, keys);
+    R.zero_state();
+    if ((s = R.normalize())) return s;
+    c.launch("k_state_in", [&] {
+        k_state_in<<<R.warps_grid(n, 8), 256, 0, c.stream>>>(R.D, R.G, flags);
+    });
+    R.iteration(0, tword, false);
+    R.merge_sample(1, 0);
+    c.launch("k_state_out", [&] {
+        k_state_out<<<static_cast<int>((n * k + 255) / 256), 256, 0, c.stream>>>(R.D, R.G, flags);
+    });
+    R.collect_stats(1);
+    if (host_stats && !g_last_stats.empty()) *host_stats = g_last_stats[0];
+    return c.finish();
+}
+
+knng_status knng_debug_sample(int64_t n, int32_t k, int32_t sample_size, uint32_t tword, uint64_t seed,
+                              const uint64_t* keys, const uint8_t* flags, uint32_t* Gn, int32_t* cn, uint32_t* Go,
+                              int32_t* co, void* workspace, size_t workspace_bytes, void* stream) {
+    knng_status s = check_common(KNNG_F32, n, 1, k, KNNG_L2SQ, sample_size);
+    if (s) return s;
+    if (!is_device_ptr(keys) || !is_device_ptr(flags) || !is_device_ptr(Gn) || !is_device_ptr(cn) ||
+        !is_device_ptr(Go) || !is_device_ptr(co))
+        return fail(KNNG_E_USAGE, "arguments must be device pointers");
+    Ctx c;
+    c.stream = static_cast<cudaStream_t>(stream);
+    Run R(c);
+    R.L = make_layout(n, 1, k, sample_size, false, true, false);
+    char* ws = nullptr;
+    if ((s = get_workspace(c, workspace, workspace_bytes, R.L.total, &ws))) return s;
+    R.D = Dims{n, 1, k, sample_size, 2 * sample_size, bucket_cap(k)};
+    R.metric = KNNG_L2SQ;
+    R.seed = seed;
+    R.bind(ws, nullptr);
+    R.zero_state();
+    cudaMemcpyAsync(R.G.keys, keys, static_cast<size_t>(n) * k * 8, cudaMemcpyDeviceToDevice, c.stream);
+    c.launch("k_state_in", [&] {
+        k_state_in<<<R.warps_grid(n, 8), 256, 0, c.stream>>>(R.D, R.G, flags);
+    });
+    R.merge_sample(0, 1);
+    R.reverse(tword);
+    c.launch("k_samples_out", [&] {
+        k_samples_out<<<static_cast<int>((n * R.D.cap + 255) / 256), 256, 0, c.stream>>>(R.D, R.S, Gn, cn, Go, co);
+    });
+    return c.finish();
+}
+
+knng_status knng_debug_philox(const uint32_t* ctr, int64_t m, uint64_t seed, uint32_t* out, void* stream) {
+    if (m < 0) return fail(KNNG_E_USAGE, "m < 0");
+    if (m == 0) return KNNG_OK;
+    if (!is_device_ptr(ctr) || !is_device_ptr(out)) return fail(KNNG_E_USAGE, "arguments must be device pointers");
+    Ctx c;
+    c.stream = static_cast<cudaStream_t>(stream);
+    c.launch("k_philox_test", [&] {
+        k_philox_test<<<static_cast<int>((m + 255) / 256), 256, 0, c.stream>>>(ctr, m, seed, out);
+    });
+    return c.finish();
+}
+
+// ------------------------------------------------------------ GGM (Alg. 3)
+size_t knng_merge_workspace_bytes(knng_dtype dt, int64_t nA, int64_t nB, int32_t d, int32_t k, int32_t sample_size,
+                                  knng_metric metric) {
+    if (check_common(dt, nA + nB, d, k, metric, sample_size) != KNNG_OK) return 0;
+    const int64_t n = nA + nB;
+    const size_t vbytes = static_cast<size_t>(n) * d * (dt == KNNG_F32 ? 4 : 1);
+    return make_layout(n, d, k, sample_size, metric == KNNG_COSINE, true, true).total + align_up(vbytes);
+}
+
+knng_status knng_merge(const void* vecA, int64_t nA, const uint32_t* idsA, const float* distsA, const void* vecB,
+                       int64_t nB, const uint32_t* idsB, const float* distsB, knng_dtype dt, int32_t d, int32_t k,
+                       knng_metric metric, int32_t merge_iters, int32_t sample_size, int32_t level, uint64_t seed,
+                       uint32_t* out_ids, float* out_dists, void* workspace, size_t workspace_bytes, void* stream) {
+    const int64_t n = nA + nB;
+    knng_status s = check_common(dt, n, d, k, metric, sample_size);
+    if (s) return s;
+    const int kr = k / 2;
+    if (nA < kr || nB < kr || nA < 1 || nB < 1)
+        return fail(KNNG_E_USAGE, "each graph needs at least floor(k/2) = %d nodes (nA=%lld, nB=%lld)", kr,
+                    static_cast<long long>(nA), static_cast<long long>(nB));
+    if (nA <= k || nB <= k) return fail(KNNG_E_USAGE, "each input graph needs n > k");
+    if (merge_iters < 0 || merge_iters > kMaxIters) return fail(KNNG_E_USAGE, "merge_iters must be in [0, %d]", kMaxIters);
+    if (level < 0 || level > 0x7FFF) return fail(KNNG_E_USAGE, "level must be in [0, 32767]");
+    if (!is_device_ptr(vecA) || !is_device_ptr(vecB) || !is_device_ptr(idsA) || !is_device_ptr(distsA) ||
+        !is_device_ptr(idsB) || !is_device_ptr(distsB) || !is_device_ptr(out_ids) || !is_device_ptr(out_dists))
+        return fail(KNNG_E_USAGE, "arguments must be device pointers");
+    Ctx c;
+    c.stream = static_cast<cudaStream_t>(stream);
+    c.timing = g_timing.load() != 0;
+    Run R(c);
+    R.L = make_layout(n, d, k, sample_size, metric == KNNG_COSINE, true, true);
+    const size_t esz = dt == KNNG_F32 ? 4 : 1;
+    const size_t vbytes = static_cast<size_t>(n) * d * esz;
+    char* ws = nullptr;
+    if ((s = get_workspace(c, workspace, workspace_bytes, R.L.total + align_up(vbytes), &ws))) return s;
+    // combined vector set [S1; S2] (S = S1 U S2)
+    char* X = ws + R.L.total;
+    cudaMemcpyAsync(X, vecA, static_cast<size_t>(nA) * d * esz, cudaMemcpyDeviceToDevice, c.stream);
+    cudaMemcpyAsync(X + static_cast<size_t>(nA) * d * esz, vecB, static_cast<size_t>(nB) * d * esz,
+                    cudaMemcpyDeviceToDevice, c.stream);
+    R.D = Dims{n, d, k, sample_size, 2 * sample_size, bucket_cap(k)};
+    R.X = X;
+    R.dt = dt;
+    R.metric = metric;
+    R.seed = seed;
+    R.boundary = nA;
+    R.bind(ws, nullptr);
+    R.zero_state();
+    if ((s = R.normalize())) return s;
+    uint64_t* reserved = reinterpret_cast<uint64_t*>(ws + R.L.reserved);
+    const int grid = R.warps_grid(n, 8);
+    c.launch("k_ggm_seed", [&] {
+        if (metric == KNNG_COSINE)
+            k_ggm_seed<float, true><<<grid, 256, 0, c.stream>>>(nullptr, R.Xn, R.D, nA, level, seed, idsA, distsA, idsB,
+                                                                distsB, R.G, reserved);
+        else if (dt == KNNG_F32)
+            k_ggm_seed<float, false><<<grid, 256, 0, c.stream>>>(reinterpret_cast<const float*>(X), nullptr, R.D, nA,
+                                                                 level, seed, idsA, distsA, idsB, distsB, R.G, reserved);
+        else
+            k_ggm_seed<uint8_t, false><<<grid, 256, 0, c.stream>>>(reinterpret_cast<const uint8_t*>(X), nullptr, R.D,
+                                                                   nA, level, seed, idsA, distsA, idsB, distsB, R.G,
+                                                                   reserved);
+    });
+    for (int t = 0; t < merge_iters; ++t)
+        R.iteration(t, 0x80000000u | (static_cast<uint32_t>(level) << 16) | static_cast<uint32_t>(t), t > 0);
+    R.merge_sample(1, 0);
+    c.launch("k_ggm_finalize", [&] {
+        k_ggm_finalize<<<grid, 256, 256 / 32 * 32 * sizeof(Elem), c.stream>>>(R.D, R.G, reserved);
+    });
+    R.export_graph(out_ids, out_dists);
+    R.collect_stats(merge_iters);
+    return c.finish();
+}
+
+// ------------------------------------------------------------ introspection
+int32_t knng_last_stats(knng_iter_stats* host_out, int32_t max_iters) {
+    const int32_t m = static_cast<int32_t>(g_last_stats.size()) < max_iters ? static_cast<int32_t>(g_last_stats.size()) : max_iters;
+    for (int32_t i = 0; i < m; ++i) host_out[i] = g_last_stats[i];
+    return m;
+}
+
+int64_t knng_launch_count(void) { return g_launches.load(); }
+
+void knng_set_timing(int32_t enable) { g_timing.store(enable ? 1 : 0); }
+
+void knng_reset_timing(void) {
+    std::lock_guard<std::mutex> lk(g_time_mu);
+    g_times.clear();
+}
+
+int32_t knng_kernel_time(const char* name, double* total_ms, int64_t* launches) {
+    std::lock_guard<std::mutex> lk(g_time_mu);
+    auto it = g_times.find(name ? name : "");
+    if (it == g_times.end()) {
+        if (total_ms) *total_ms = 0.0;
+        if (launches) *launches = 0;
+        return 0;
+    }
+    if (total_ms) *total_ms = it->second.first;
+    if (launches) *launches = it->second.second;
+    return 1;
+}
+
+const char* knng_last_error(void) { return g_err.c_str(); }
+
+const char* knng_status_string(knng_status s) {
+    switch (s) {
+        case KNNG_OK: return "KNNG_OK";
+        case KNNG_E_USAGE: return "KNNG_E_USAGE";
+        case KNNG_E_DOMAIN: return "KNNG_E_DOMAIN";
+        case KNNG_E_NOMEM: return "KNNG_E_NOMEM";
+        case KNNG_E_CUDA: return "KNNG_E_CUDA";
+        case KNNG_E_NCCL: return "KNNG_E_NCCL";
+        case KNNG_E_INTERNAL: return "KNNG_E_INTERNAL";
+    }
+    return "unknown";
+}
+
+int32_t knng_abi_version(void) { return 1; }
+
+}  // extern "C"

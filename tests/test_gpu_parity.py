@@ -1,0 +1,177 @@
+"""Parity of the CUDA path (through the C ABI) with the oracle, element by
+element on seeded inputs.  Integer/index work (ids, flags, sample tables)
+must match bit-exactly; distances too, because both sides evaluate the
+canonical order of DESIGN.md D5/D6 (the tolerance of BASELINE.json --
+1e-5 relative -- is therefore met with zero error)."""
+import os
+
+import numpy as np
+import pytest
+
+import datagen
+import oracle.oracle as orc
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.fixture(scope="module")
+def K():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2103_15386_b200.knng as K
+    K.lib()
+    return K
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def u64(t):
+    return t.cpu().numpy().view(np.uint64)
+
+
+# ------------------------------------------------------------------ Philox
+def test_device_philox_known_answers(K):
+    rows = [l.split() for l in open(os.path.join(GOLDEN, "philox_kat.txt")) if l.strip() and not l.startswith("#")]
+    for r in rows:
+        if r[0] == "cxx26":
+            block, seed, word, expect = (int(x) for x in r[1:])
+            out = K.knng_debug_philox(dev(np.array([[block, 0, 0, 0]], np.int32)), seed)
+            assert int(out.cpu().numpy().view(np.uint32)[0, word]) == expect
+            continue
+        v = [int(x, 16) for x in r]
+        seed = v[4] | (v[5] << 32)
+        ctr = dev(np.array([v[0:4]], np.uint32).view(np.int32))
+        out = K.knng_debug_philox(ctr, seed).cpu().numpy().view(np.uint32)[0]
+        assert list(out) == v[6:10]
+    # bulk agreement with the oracle generator
+    rng = np.random.default_rng(0)
+    ctr = rng.integers(0, 2**32, size=(512, 4), dtype=np.uint64).astype(np.uint32)
+    out = K.knng_debug_philox(dev(ctr.view(np.int32)), 0x1234_5678_9ABC).cpu().numpy().view(np.uint32)
+    for i in range(0, 512, 37):
+        assert list(out[i]) == list(orc.philox(ctr[i], [0x56789ABC, 0x1234]))
+
+
+# ------------------------------------------------------------------ init
+CASES = [
+    # (shape, n, d, k, p, dtype, metric)
+    ("c1", 10000, 16, 10, 8, "f32", "l2"),       # BASELINE configs[0]
+    ("sift", 6000, 128, 32, 16, "f32", "l2"),    # SIFT-shaped, 4 slabs
+    ("sift", 3000, 128, 32, 16, "u8", "l2"),     # uint8 path (C5 dtype)
+    ("c1", 2500, 100, 20, 7, "f32", "l2"),       # ragged d (last slab partial)
+    ("c1", 1500, 7, 8, 3, "f32", "l2"),          # rows not 16-B aligned
+    ("deep", 3000, 96, 16, 8, "f32", "cosine"),  # cosine (D6)
+    ("uniform", 40, 3, 2, 1, "f32", "l2"),       # k=2, p=1 degenerate
+    ("uniform", 33, 5, 32, 16, "f32", "l2"),     # n = k + 1 (every list is all others)
+]
+
+
+def _data(shape, n, d, dtype, seed=3):
+    if shape == "sift":
+        return datagen.make("sift", n, seed=seed, dtype=dtype)
+    return datagen.make(shape, n, seed=seed, d=d)
+
+
+def _metric(m):
+    return orc.COSINE if m == "cosine" else orc.L2SQ
+
+
+@pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}-{c[1]}-{c[2]}-{c[3]}-{c[5]}-{c[6]}" for c in CASES])
+def test_init_bit_exact(K, case):
+    shape, n, d, k, p, dtype, metric = case
+    X = _data(shape, n, d, dtype)
+    ok, of = orc.init(X, k, 42, _metric(metric))
+    gk, gf = K.knng_debug_init(dev(X), k, 42, metric)
+    assert np.array_equal(u64(gk), ok)
+    assert np.array_equal(gf.cpu().numpy(), of)
+
+
+# ------------------------------------------------------------------ sampling
+@pytest.mark.parametrize("n,k,p,seed", [(2000, 10, 8, 0), (5000, 32, 16, 1), (300, 6, 2, 2), (1000, 20, 13, 3)])
+def test_sample_tables_bit_exact(K, n, k, p, seed):
+    rng = np.random.default_rng(seed)
+    X = datagen.make("c1", n, seed=seed, d=4)
+    keys, flags = orc.init(X, k, seed)
+    # a mixed NEW/OLD state after two iterations, plus random flags
+    for t in range(2):
+        orc.iterate(X, keys, flags, p, t, seed)
+    flags = (rng.random(flags.shape) < 0.5).astype(np.uint8)
+    tword = 0x80000000 | 5 if seed % 2 else 3
+    s = orc.sample(keys, flags, p, tword, 99)
+    Gn, cn, Go, co = K.knng_debug_sample(dev(keys.view(np.int64)), dev(flags), p, tword, 99)
+    cn, co = cn.cpu().numpy(), co.cpu().numpy()
+    assert np.array_equal(cn, s["cn"]) and np.array_equal(co, s["co"])
+    Gn, Go = Gn.cpu().numpy().view(np.uint32), Go.cpu().numpy().view(np.uint32)
+    for v in range(n):
+        assert np.array_equal(Gn[v, :cn[v]], s["Gn"][v, :cn[v]])
+        assert np.array_equal(Go[v, :co[v]], s["Go"][v, :co[v]])
+
+
+# ------------------------------------------------------ iterations (teacher forced)
+@pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}-{c[1]}-{c[2]}-{c[3]}-{c[5]}-{c[6]}" for c in CASES])
+def test_iterations_teacher_forced_bit_exact(K, case):
+    shape, n, d, k, p, dtype, metric = case
+    X = _data(shape, n, d, dtype)
+    m = _metric(metric)
+    Xd = dev(X)
+    keys, flags = orc.init(X, k, 7, m)
+    for t in range(6):
+        gk, gf = dev(keys.view(np.int64)), dev(flags)
+        st = K.knng_debug_iterate(Xd, gk, gf, p, t, 7, -1, metric)
+        ost = orc.iterate(X, keys, flags, p, t, 7, m)
+        assert np.array_equal(u64(gk), keys), f"keys differ at iteration {t}"
+        assert np.array_equal(gf.cpu().numpy(), flags), f"flags differ at iteration {t}"
+        assert st["dist_evals"] == ost["dist_evals"]
+        assert st["joins"] == ost["joins"] and st["sum_m"] == ost["sum_m"] and st["sum_q"] == ost["sum_q"]
+        assert st["candidates"] == ost["candidates"]
+
+
+@pytest.mark.parametrize("case", CASES[:3] + CASES[5:6], ids=lambda c: f"{c[0]}-{c[1]}-{c[5]}-{c[6]}")
+def test_full_build_bit_exact(K, case):
+    shape, n, d, k, p, dtype, metric = case
+    X = _data(shape, n, d, dtype)
+    iters = 8
+    oi, od = orc.build(X, k, p, iters, 11, _metric(metric))
+    gi, gd = K.knng_build(dev(X), k, iters, p, 11, metric)
+    assert np.array_equal(gi.cpu().numpy().view(np.uint32), oi)
+    assert np.array_equal(gd.cpu().numpy(), od)  # canonical order: 0 error
+    # and the end-to-end host entry point gives the same graph
+    hi, hd = K.knng_build_host(np.ascontiguousarray(X), k, iters, p, 11, metric)
+    assert np.array_equal(hi, oi) and np.array_equal(hd, od)
+
+
+def test_c1_end_to_end_recall_matches_oracle(K):
+    # BASELINE configs[0]: n=10k GMM d=16, k=10, p=8, 10 iterations
+    X = datagen.make("c1", 10000, seed=1)
+    q = datagen.sample_nodes(10000, 2000)
+    gt = orc.bruteforce(X, q, 10)
+    oi, od = orc.build(X, 10, 8, 10, 42)
+    gi, gd = K.knng_build(dev(X), 10, 10, 8, 42)
+    gkeys = orc.key(gd.cpu().numpy(), gi.cpu().numpy().view(np.uint32))
+    r_gpu = orc.recall(gkeys[q], gt, 10)
+    r_orc = orc.recall(orc.key(od, oi)[q], gt, 10)
+    assert abs(r_gpu - r_orc) <= 0.005
+    assert r_gpu >= 0.94
+
+
+def test_determinism_two_runs(K):
+    X = dev(datagen.make("sift", 20000, seed=5))
+    a = K.knng_build(X, 32, 6, 16, 3)
+    b = K.knng_build(X, 32, 6, 16, 3)
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+# ------------------------------------------------------------------ eval
+@pytest.mark.parametrize("shape,n,d,dtype,metric", [("c1", 3000, 16, "f32", "l2"), ("sift", 4000, 128, "u8", "l2"),
+                                                    ("deep", 2000, 96, "f32", "cosine"), ("c1", 1000, 7, "f32", "l2")])
+def test_bruteforce_bit_exact(K, shape, n, d, dtype, metric):
+    X = _data(shape, n, d, dtype)
+    q = np.arange(0, n, 13, dtype=np.int64)
+    o = orc.bruteforce(X, q, 10, _metric(metric))
+    gi, gd = K.knng_bruteforce(dev(X), dev(q), 10, metric)
+    assert np.array_equal(gi.cpu().numpy().view(np.uint32), orc.key_ids(o))
+    assert np.array_equal(gd.cpu().numpy(), orc.key_dists(o))
