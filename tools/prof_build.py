@@ -1,0 +1,29 @@
+"""One SIFT1M-shaped GNND build for profiling under ncu (never a bench value).
+
+  ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+      --log-file gpurun_out/launches.csv python tools/prof_build.py
+  ncu --set full --clock-control none --import-source on -k regex:k_join \
+      -s 3 -c 1 -o gpurun_out/join python tools/prof_build.py
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import datagen  # noqa: E402
+import paper_2103_15386_b200.knng as K  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--n", type=int, default=1_000_000)
+ap.add_argument("--k", type=int, default=32)
+ap.add_argument("--p", type=int, default=16)
+ap.add_argument("--iters", type=int, default=8)
+ap.add_argument("--builds", type=int, default=1)
+a = ap.parse_args()
+X = torch.from_numpy(datagen.make("sift", a.n, seed=1)).cuda()
+for _ in range(a.builds):
+    K.knng_build(X, a.k, a.iters, a.p, 42)
+torch.cuda.synchronize()
+print("stats", K.knng_last_stats())
