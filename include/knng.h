@@ -62,8 +62,9 @@ typedef struct {
     int64_t dist_evals;   /* distances the method needs: m(m-1)/2 + m q per
                              join (only cross pairs in a GGM refine)           */
     int64_t candidates;   /* non-sentinel GetNearestObject results (Alg. 2)    */
-    int64_t appended;     /* candidates below the target's k-th key          */
-    int64_t overflow;     /* of those, inserted by the locked path            */
+    int64_t appended;     /* candidates below the target's k-th key (filed
+                             into its bucket)                                */
+    int64_t accepted;     /* list entries that are new after the update      */
     int64_t rows;         /* vector rows gathered by the join kernel          */
 } knng_iter_stats;
 

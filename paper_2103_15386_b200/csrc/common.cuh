@@ -126,10 +126,10 @@ __device__ __forceinline__ Elem warp_bitonic_merge_elem(Elem x) {
 // Merge one chunk of up to 32 candidate keys (one per lane, any order, may
 // repeat, kSentinel = empty) into a sorted unique list held one entry per
 // lane (lanes >= its length hold kSentinel).  Result: the 32 smallest unique
-// keys of the union, ascending; list entries keep their NEW flag, newcomers
-// are NEW.  scratch: 32 Elem of per-warp shared memory.  Returns the number
-// of newcomers that entered.
-__device__ __forceinline__ int warp_merge_chunk(Elem& cur, uint64_t cand, Elem* scratch) {
+// keys of the union, ascending; list entries keep their NEW flag and origin
+// bit, newcomers are NEW with origin = candidate.  scratch: 32 Elem of
+// per-warp shared memory.
+__device__ __forceinline__ void warp_merge_chunk(Elem& cur, uint64_t cand, Elem* scratch) {
     const uint32_t lane = lane_id();
     Elem b{cand, 3u};  // origin = candidate, NEW
     b = warp_sort_elem(b);
@@ -159,9 +159,6 @@ __device__ __forceinline__ int warp_merge_chunk(Elem& cur, uint64_t cand, Elem* 
     __syncwarp();
     cur = scratch[lane];
     __syncwarp();
-    const bool entered = cur.key != kSentinel && (cur.meta >> 1) != 0;
-    cur.meta &= 1u;  // the merged list is all "list origin" from now on
-    return __popc(__ballot_sync(kFull, entered));
 }
 
 // ---------------------------------------------------------------- distances

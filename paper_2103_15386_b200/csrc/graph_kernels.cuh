@@ -8,32 +8,38 @@
 namespace knng {
 
 struct DevStats {  // device mirror of knng_iter_stats
-    unsigned long long joins, sum_m, sum_q, dist_evals, candidates, appended, overflow, rows;
+    unsigned long long joins, sum_m, sum_q, dist_evals, candidates, appended, accepted, rows;
 };
 
+// Bucketed bulk update (D17): the candidates of one iteration for target t
+// live in bucket[boff[t] .. boff[t] + bcnt[t]); boff is an exclusive scan of
+// an exact upper bound of what t can receive (see k_scan_*), so a bucket can
+// never overflow and no lock is needed.
 struct Graph {
     uint64_t* keys;     // [n][k] ascending
     uint32_t* newmask;  // [n]    bit j = entry j is NEW
     uint64_t* kth;      // [n]    k-th key at iteration start (update threshold)
-    uint32_t* lock;     // [n]    spinlock of the overflow insert path
-    uint32_t* bcnt;     // [n]    candidates appended to the bucket
-    uint64_t* bucket;   // [n][B] candidate keys of the current iteration
+    uint32_t* bcnt;     // [n]    candidates appended to t's bucket
+    const uint64_t* boff;  // [n+1] bucket offsets (= Samples::off channel 2)
+    uint64_t* bucket;   // [6 n p] candidate keys of the current iteration
 };
 
 struct Samples {
     uint32_t* fwd;   // [2][n][p]   forward NEW / OLD samples
     uint8_t* fcnt;   // [n][2]
-    uint32_t* rcnt;  // [2][n]      reverse counts, then cursors
-    uint32_t* roff;  // [2][n+1]    reverse CSR offsets
+    uint32_t* rcnt;  // [2][n]      reverse counts
+    uint32_t* rcur;  // [2][n]      reverse scatter cursors
+    uint64_t* off;   // [3][n+1]    CSR offsets: reverse NEW, reverse OLD, buckets
     uint32_t* rsrc;  // [2][n*p]    reverse sources
     uint32_t* G;     // [2][n][cap] G_new / G_old, sorted unique
     uint8_t* gcnt;   // [n][2]      m = |G_new|, q = |G_old|
-    uint32_t* bsum;  // [2][nblk]   scan block sums
+    uint64_t* bsum;  // [3][nblk]   scan block sums
+    uint64_t* cand;  // [n][3 cap]  join output: c_nn(u), c_no(u), c_on(w) keys
 };
 
 struct Dims {
     int64_t n;
-    int d, k, p, cap, B;
+    int d, k, p, cap;
 };
 
 __device__ __forceinline__ uint32_t kmask_of(int k) { return k >= 32 ? kFull : ((1u << k) - 1u); }
@@ -96,7 +102,8 @@ __global__ void k_init(const T* __restrict__ X, const float* __restrict__ Xn, Di
 //             FO(s) = first min(p, #OLD) OLD entries in list order (P:147,
 //             D7); FN entries are marked OLD (D12-D13); reverse counts
 //             for the CSR of P:149.
-__global__ void k_merge_sample(Dims D, Graph G, Samples S, int do_merge, int do_sample) {
+__global__ void k_merge_sample(Dims D, Graph G, Samples S, int do_merge, int do_sample,
+                               DevStats* __restrict__ prev_stats) {
     extern __shared__ Elem smem_scratch[];
     const int64_t s = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (s >= D.n) return;
@@ -109,16 +116,21 @@ __global__ void k_merge_sample(Dims D, Graph G, Samples S, int do_merge, int do_
              in_list ? ((mask >> lane) & 1u) : 0u};
     bool changed = false;
     if (do_merge) {
-        const uint32_t c = min(G.bcnt[s], static_cast<uint32_t>(D.B));
-        for (uint32_t base = 0; base < c; base += 32) {
-            const uint64_t cand = (base + lane < c) ? G.bucket[static_cast<size_t>(s) * D.B + base + lane] : kSentinel;
-            warp_merge_chunk(cur, cand, scratch);
-        }
+        const uint32_t c = G.bcnt[s];
         if (c > 0) {
+            const uint64_t* bk = G.bucket + G.boff[s];
+            for (uint32_t base = 0; base < c; base += 32) {
+                const uint64_t cand = (base + lane < c) ? bk[base + lane] : kSentinel;
+                warp_merge_chunk(cur, cand, scratch);
+            }
             changed = true;
             if (!in_list) cur = Elem{kSentinel, 0u};
+            // newcomers that made it into the k-list (oracle's "accepted")
+            const uint32_t acc = __ballot_sync(kFull, in_list && (cur.meta >> 1));
+            if (lane == 0 && acc && prev_stats) atomicAdd(&prev_stats->accepted, static_cast<unsigned long long>(__popc(acc)));
+            cur.meta &= 1u;
+            if (lane == 0) G.bcnt[s] = 0;
         }
-        if (lane == 0) G.bcnt[s] = 0;
     }
     if (do_sample) {
         const bool isnew = in_list && (cur.meta & 1u);
@@ -148,25 +160,31 @@ __global__ void k_merge_sample(Dims D, Graph G, Samples S, int do_merge, int do_
     if (static_cast<int>(lane) == k - 1) G.kth[s] = cur.key;
 }
 
-// ------------------------------------------------- reverse CSR
-// Exclusive scan of rcnt[2][n] into roff[2][n+1]; the counts are zeroed so
-// they serve as scatter cursors.  Three phases, 1024 items per block.
+// ------------------------------------------------- CSR offsets
+// Exclusive scans (u64) of three per-node counts into S.off[3][n+1]:
+//   channel 0/1: reverse NEW / OLD counts (CSR of the reverse appends)
+//   channel 2  : bucket capacity of target t, an exact upper bound of the
+//                candidates t can receive this iteration: t is in G_new(x)
+//                only if x in R_new(t) or x in F_new(t), and gets <= 2 keys
+//                from such a join; in G_old(x) only if x in R_old(t) or
+//                F_old(t), <= 1 key (Alg. 1 lines 12-31).
+// Three phases, 1024 items per block.
 constexpr int kScanBlock = 1024;
 
-__device__ __forceinline__ uint32_t block_inclusive_scan(uint32_t v, uint32_t* warp_tot) {
+__device__ __forceinline__ uint64_t block_inclusive_scan(uint64_t v, uint64_t* warp_tot) {
     const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(kFull, v, o);
+        const uint64_t t = __shfl_up_sync(kFull, v, o);
         if (lane >= static_cast<uint32_t>(o)) v += t;
     }
     if (lane == 31) warp_tot[w] = v;
     __syncthreads();
     if (w == 0) {
-        uint32_t x = lane < (blockDim.x >> 5) ? warp_tot[lane] : 0u;
+        uint64_t x = lane < (blockDim.x >> 5) ? warp_tot[lane] : 0ull;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(kFull, x, o);
+            const uint64_t t = __shfl_up_sync(kFull, x, o);
             if (lane >= static_cast<uint32_t>(o)) x += t;
         }
         warp_tot[lane] = x;
@@ -176,43 +194,45 @@ __device__ __forceinline__ uint32_t block_inclusive_scan(uint32_t v, uint32_t* w
     return v;
 }
 
-__global__ void k_scan_reduce(const uint32_t* __restrict__ cnt, int64_t n, uint32_t* bsum, int64_t nblk) {
-    __shared__ uint32_t wt[32];
-    const int f = blockIdx.y;
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * kScanBlock + threadIdx.x;
-    uint32_t v = i < n ? cnt[f * n + i] : 0u;
-    v = block_inclusive_scan(v, wt);
-    if (threadIdx.x == kScanBlock - 1) bsum[f * nblk + blockIdx.x] = v;
+__device__ __forceinline__ uint64_t scan_item(const Samples& S, int64_t n, int f, int64_t i) {
+    if (i >= n) return 0ull;
+    if (f < 2) return S.rcnt[f * n + i];
+    return 2ull * (S.rcnt[i] + S.fcnt[2 * i]) + S.rcnt[n + i] + S.fcnt[2 * i + 1];
 }
 
-__global__ void k_scan_bsums(uint32_t* bsum, int64_t nblk) {
-    __shared__ uint32_t wt[32];
-    const int f = blockIdx.x;
-    uint32_t* b = bsum + f * nblk;
+__global__ void k_scan_reduce(Samples S, int64_t n, int64_t nblk) {
+    __shared__ uint64_t wt[32];
+    const int f = blockIdx.y;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * kScanBlock + threadIdx.x;
+    const uint64_t v = block_inclusive_scan(scan_item(S, n, f, i), wt);
+    if (threadIdx.x == kScanBlock - 1) S.bsum[f * nblk + blockIdx.x] = v;
+}
+
+__global__ void k_scan_bsums(uint64_t* bsum, int64_t nblk) {
+    __shared__ uint64_t wt[32];
+    uint64_t* b = bsum + blockIdx.x * nblk;
     const int64_t per = (nblk + kScanBlock - 1) / kScanBlock;
     const int64_t lo = threadIdx.x * per, hi = min(nblk, lo + per);
-    uint32_t sum = 0;
+    uint64_t sum = 0;
     for (int64_t i = lo; i < hi; ++i) sum += b[i];
-    const uint32_t incl = block_inclusive_scan(sum, wt);
-    uint32_t run = incl - sum;
+    const uint64_t incl = block_inclusive_scan(sum, wt);
+    uint64_t run = incl - sum;
     for (int64_t i = lo; i < hi; ++i) {
-        const uint32_t x = b[i];
+        const uint64_t x = b[i];
         b[i] = run;
         run += x;
     }
 }
 
-__global__ void k_scan_final(uint32_t* cnt, int64_t n, const uint32_t* __restrict__ bsum, int64_t nblk,
-                             uint32_t* off) {
-    __shared__ uint32_t wt[32];
+__global__ void k_scan_final(Samples S, int64_t n, int64_t nblk) {
+    __shared__ uint64_t wt[32];
     const int f = blockIdx.y;
     const int64_t i = static_cast<int64_t>(blockIdx.x) * kScanBlock + threadIdx.x;
-    const uint32_t v = i < n ? cnt[f * n + i] : 0u;
-    const uint32_t incl = block_inclusive_scan(v, wt) + bsum[f * nblk + blockIdx.x];
+    const uint64_t v = scan_item(S, n, f, i);
+    const uint64_t incl = block_inclusive_scan(v, wt) + S.bsum[f * nblk + blockIdx.x];
     if (i < n) {
-        off[f * (n + 1) + i] = incl - v;
-        cnt[f * n + i] = 0u;
-        if (i == n - 1) off[f * (n + 1) + n] = incl;
+        S.off[f * (n + 1) + i] = incl - v;
+        if (i == n - 1) S.off[f * (n + 1) + n] = incl;
     }
 }
 
@@ -227,8 +247,8 @@ __global__ void k_rev_scatter(Dims D, Samples S) {
     const int j = static_cast<int>(i - s * D.p);
     if (j >= S.fcnt[2 * s + f]) return;
     const uint32_t v = S.fwd[static_cast<size_t>(f) * D.n * D.p + i];
-    const uint32_t pos = atomicAdd(S.rcnt + f * D.n + v, 1u);
-    S.rsrc[static_cast<size_t>(f) * D.n * D.p + S.roff[f * (D.n + 1) + v] + pos] = static_cast<uint32_t>(s);
+    const uint32_t pos = atomicAdd(S.rcur + f * D.n + v, 1u);
+    S.rsrc[static_cast<size_t>(f) * D.n * D.p + S.off[f * (D.n + 1) + v] + pos] = static_cast<uint32_t>(s);
 }
 
 __device__ __forceinline__ uint64_t warp_bitonic_merge_u64(uint64_t x) {
@@ -273,7 +293,7 @@ __global__ void k_rev_select(Dims D, Samples S, uint32_t tword, uint64_t seed) {
         const int fc = S.fcnt[2 * v + f];
         const uint32_t* fwd = S.fwd + static_cast<size_t>(f) * D.n * p + static_cast<size_t>(v) * p;
         const uint32_t* rs = S.rsrc + static_cast<size_t>(f) * D.n * p;
-        const uint32_t o0 = S.roff[f * (D.n + 1) + v], o1 = S.roff[f * (D.n + 1) + v + 1];
+        const uint64_t o0 = S.off[f * (D.n + 1) + v], o1 = S.off[f * (D.n + 1) + v + 1];
         const int r = static_cast<int>(o1 - o0);
         const int c = cap - fc;
         uint32_t e = 0xFFFFFFFFu;
@@ -317,7 +337,8 @@ __global__ void k_rev_select(Dims D, Samples S, uint32_t tword, uint64_t seed) {
         if (static_cast<int>(lane) < cnt) S.G[static_cast<size_t>(f) * D.n * cap + static_cast<size_t>(v) * cap + lane] = u;
         if (lane == 0) {
             S.gcnt[2 * v + f] = static_cast<uint8_t>(cnt);
-            S.rcnt[f * D.n + v] = 0u;  // cursors back to zero for the next iteration
+            S.rcnt[f * D.n + v] = 0u;  // counts and cursors back to zero
+            S.rcur[f * D.n + v] = 0u;
         }
     }
 }
@@ -342,7 +363,6 @@ __global__ void k_state_in(Dims D, Graph G, const uint8_t* __restrict__ flags) {
     if (lane == 0) {
         G.newmask[s] = nm;
         G.bcnt[s] = 0;
-        G.lock[s] = 0;
         G.kth[s] = G.keys[static_cast<size_t>(s) * D.k + D.k - 1];
     }
 }

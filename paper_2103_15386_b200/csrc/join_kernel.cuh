@@ -1,23 +1,26 @@
 // join_kernel.cuh -- the local join of Alg. 1.
 //
-// One CTA (128 threads) per node x with m = |G_new(x)| > 0.
+// k_join: one CTA (128 threads) per node x with m = |G_new(x)| > 0,
+// persistent over nodes.
 //  gather : the m NEW and q OLD sample rows are staged into shared memory
 //           with cp.async 16-B copies (L2-only .cg), slab by slab over the
-//           dimensions (SLAB = 32 dims per stage, double-buffered), so any d
-//           works with a fixed shared-memory footprint ("sub-vectors").
+//           dimensions (32 dims per stage, double-buffered), so any d works
+//           with a fixed shared-memory footprint ("sub-vectors").
 //  tile   : the CalculateDistances tile of P:181-194 as a register-blocked
 //           contraction: each thread owns a 4x4 block of (NEW row, sample
 //           column) pairs, lower-triangular blocks for NEW-NEW, all blocks
 //           for NEW-OLD.  Every pair keeps one accumulator and walks the
-//           dimensions in order, which is exactly the canonical distance of
-//           D5/D6 -- results are bit-identical to the oracle's.
+//           dimensions in order: exactly the canonical distance of D5/D6, so
+//           results are bit-identical to the oracle's.
 //  select : GetNearestObject (Alg. 2) as packed (dist, id) u64 minima: a
 //           per-thread pre-reduction then shared-memory atomicMin -- the
 //           paper's atomicMin on (v, d) with the (dist, id) order D3.
-//  update : each selected candidate below its target's iteration-start k-th
-//           key (an exact filter, D17) is appended to the target's bucket;
-//           a full bucket falls back to the paper's locked insertion into
-//           the list.  Buckets are merged by k_merge_sample.
+//  output : the 2m + q selected keys go to a fixed per-node slot range of
+//           S.cand (coalesced, no atomics); k_cand_scatter files them.
+//
+// k_cand_scatter: one thread per candidate slot: drops keys that cannot
+// enter (>= the target's iteration-start k-th key: exact, D17) and appends
+// the rest to the target's CSR bucket (never overflows, see k_scan_*).
 #pragma once
 #include <type_traits>
 
@@ -55,53 +58,10 @@ __device__ __forceinline__ bool allowed_pair(int64_t boundary, uint32_t a, uint3
     return boundary < 0 || ((static_cast<int64_t>(a) >= boundary) != (static_cast<int64_t>(b) >= boundary));
 }
 
-// InsertIntoNNList under the per-list spinlock: the overflow path
-// of a full bucket.  Order-independent with the bucket merge (D17).
-__device__ void locked_insert(Graph G, int k, uint32_t t, uint64_t key) {
-    uint32_t* lk = G.lock + t;
-    while (atomicCAS(lk, 0u, 1u) != 0u) __nanosleep(40);
-    __threadfence();
-    uint64_t* L = G.keys + static_cast<size_t>(t) * k;
-    if (key < __ldcg(L + k - 1)) {
-        bool dup = false;
-        int below = 0;
-        for (int j = 0; j < k; ++j) {
-            const uint64_t lj = __ldcg(L + j);
-            dup |= key_id(lj) == key_id(key);
-            below += lj < key ? 1 : 0;
-        }
-        if (!dup) {
-            for (int j = k - 1; j > below; --j) __stcg(L + j, __ldcg(L + j - 1));
-            __stcg(L + below, key);
-            const uint32_t m = __ldcg(G.newmask + t);
-            const uint32_t lowm = (1u << below) - 1u;
-            const uint32_t nm = ((m & lowm) | (1u << below) | ((m << 1) & ~(lowm | (1u << below)))) & kmask_of(k);
-            __stcg(G.newmask + t, nm);
-        }
-    }
-    __threadfence();
-    atomicExch(lk, 0u);
-}
-
-__device__ __forceinline__ void emit_candidate(Graph G, int k, int B, uint32_t target, uint64_t key,
-                                               unsigned int* c_cand, unsigned int* c_app, unsigned int* c_ovf) {
-    if (key == kSentinel) return;  // D15
-    atomicAdd(c_cand, 1u);
-    if (!(key < __ldg(G.kth + target))) return;  // cannot enter (exact, D17)
-    atomicAdd(c_app, 1u);
-    const uint32_t slot = atomicAdd(G.bcnt + target, 1u);
-    if (slot < static_cast<uint32_t>(B)) {
-        G.bucket[static_cast<size_t>(target) * B + slot] = key;
-    } else {
-        atomicAdd(c_ovf, 1u);
-        locked_insert(G, k, target, key);
-    }
-}
-
 template <typename T, bool COS>
 __global__ void __launch_bounds__(kJoinThreads)
-k_join(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G, Samples S,
-       int64_t boundary, int aligned16, DevStats* __restrict__ stats) {
+k_join(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Samples S, int64_t boundary,
+       int aligned16, DevStats* __restrict__ stats) {
     using Cfg = SlabCfg<T>;
     using E = typename std::conditional<COS, float, T>::type;
     constexpr int SD = Cfg::kDims, RS = Cfg::kStride, CE = Cfg::kChunkElems;
@@ -111,11 +71,12 @@ k_join(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G, S
     __shared__ __align__(16) E rows[2][kMaxSlots * RS];
     __shared__ uint32_t ids[kMaxSlots];
     __shared__ unsigned long long mn_nn[32], mn_no[32], mn_on[32];
-    __shared__ unsigned int c_pairs, c_cand, c_app, c_ovf;
+    __shared__ unsigned int c_pairs;
 
     const int tid = threadIdx.x;
     const int d = D.d, cap = D.cap;
     const int nslab = (d + SD - 1) / SD;
+    unsigned long long my_joins = 0, my_m = 0, my_q = 0;
 
     for (int64_t x = blockIdx.x; x < D.n; x += gridDim.x) {
         const int m = S.gcnt[2 * x], q = S.gcnt[2 * x + 1];
@@ -123,7 +84,7 @@ k_join(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G, S
         const int mpad = (m + 3) & ~3, qpad = (q + 3) & ~3;
         const int mg = mpad >> 2, qg = qpad >> 2;
         const int nslots = mpad + qpad;
-        __syncthreads();  // previous node's smem fully consumed
+        __syncthreads();  // previous node's shared memory fully consumed
         if (tid < kMaxSlots) {
             uint32_t id = 0xFFFFFFFFu;
             if (tid < m) id = S.G[static_cast<size_t>(x) * cap + tid];
@@ -136,10 +97,10 @@ k_join(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G, S
             mn_no[tid] = kSentinel;
             mn_on[tid] = kSentinel;
         }
-        if (tid == 0) { c_pairs = 0; c_cand = 0; c_app = 0; c_ovf = 0; }
+        if (tid == 0) c_pairs = 0;
         __syncthreads();
 
-        // block assignment: NN lower-triangular blocks, then NO blocks
+        // block assignment: NN lower-triangular blocks (I >= J), then NO blocks
         const int nnn = mg * (mg + 1) / 2;
         const int nb = nnn + mg * qg;
         int I = 0, J = 0;
@@ -156,9 +117,10 @@ k_join(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G, S
                 J = mg + t2 % qg;
             }
         }
-        // column slot base: NN columns are NEW slots, NO columns start at mpad
+        const bool nn = J < mg;
         const int rbase = 4 * I;
-        const int cbase = (J < mg) ? 4 * J : mpad + 4 * (J - mg);
+        const int cbase = nn ? 4 * J : mpad + 4 * (J - mg);
+        const int aoff = rbase * RS, boff = cbase * RS;
 
         float acc[4][4];
         unsigned int iacc[4][4];
@@ -200,15 +162,16 @@ k_join(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G, S
             }
             __syncthreads();
             if (active) {
-                const E* R = rows[sl & 1];
+                const E* __restrict__ A = rows[sl & 1] + aoff;
+                const E* __restrict__ B = rows[sl & 1] + boff;
                 if constexpr (std::is_same<E, float>::value) {
-#pragma unroll 2
+#pragma unroll
                     for (int i = 0; i < SD; i += 4) {
                         float4 a[4], b[4];
 #pragma unroll
-                        for (int r = 0; r < 4; ++r) a[r] = *reinterpret_cast<const float4*>(R + (rbase + r) * RS + i);
+                        for (int r = 0; r < 4; ++r) a[r] = *reinterpret_cast<const float4*>(A + r * RS + i);
 #pragma unroll
-                        for (int c = 0; c < 4; ++c) b[c] = *reinterpret_cast<const float4*>(R + (cbase + c) * RS + i);
+                        for (int c = 0; c < 4; ++c) b[c] = *reinterpret_cast<const float4*>(B + c * RS + i);
 #pragma unroll
                         for (int r = 0; r < 4; ++r)
 #pragma unroll
@@ -229,13 +192,13 @@ k_join(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G, S
                     }
                 } else {
                     // uint8: exact integer sum of squares (D5), 4 dims per step
-#pragma unroll 2
+#pragma unroll
                     for (int i = 0; i < SD; i += 4) {
                         uint32_t a[4], b[4];
 #pragma unroll
-                        for (int r = 0; r < 4; ++r) a[r] = *reinterpret_cast<const uint32_t*>(R + (rbase + r) * RS + i);
+                        for (int r = 0; r < 4; ++r) a[r] = *reinterpret_cast<const uint32_t*>(A + r * RS + i);
 #pragma unroll
-                        for (int c = 0; c < 4; ++c) b[c] = *reinterpret_cast<const uint32_t*>(R + (cbase + c) * RS + i);
+                        for (int c = 0; c < 4; ++c) b[c] = *reinterpret_cast<const uint32_t*>(B + c * RS + i);
 #pragma unroll
                         for (int r = 0; r < 4; ++r)
 #pragma unroll
@@ -251,7 +214,6 @@ k_join(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G, S
 
         // ---- selection (Alg. 2): per-thread pre-reduction + smem atomicMin
         if (active) {
-            const bool nn = J < mg;
             unsigned pairs = 0;
             uint64_t colbest[4] = {kSentinel, kSentinel, kSentinel, kSentinel};
 #pragma unroll
@@ -261,9 +223,7 @@ k_join(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G, S
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     const int w = cbase + c;
-                    bool valid;
-                    if (nn) valid = u < m && w < u;
-                    else valid = u < m && (w - mpad) < q;
+                    bool valid = nn ? (u < m && w < u) : (u < m && (w - mpad) < q);
                     if (valid) valid = allowed_pair(boundary, ids[u], ids[w]);
                     if (!valid) continue;
                     float dist;
@@ -297,28 +257,64 @@ k_join(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G, S
         }
         __syncthreads();
 
-        // ---- update: NEW sample u gets nearest other NEW and nearest OLD
-        // (Alg. 1 lines 12-25); OLD sample gets nearest NEW (lines 26-31).
-        if (tid < m) {
-            const uint32_t u = ids[tid];
-            emit_candidate(G, D.k, D.B, u, mn_nn[tid], &c_cand, &c_app, &c_ovf);
-            emit_candidate(G, D.k, D.B, u, mn_no[tid], &c_cand, &c_app, &c_ovf);
+        // ---- output: slot j of node x holds c_nn(u_j) (j < m), c_no(u_j)
+        // (m <= j < 2m), c_on(w_j) (2m <= j < 2m + q)  (Alg. 1 lines 12-31)
+        uint64_t* out = S.cand + static_cast<size_t>(x) * (3 * cap);
+        const int total = 2 * m + q;
+        for (int j = tid; j < total; j += kJoinThreads) {
+            uint64_t v;
+            if (j < m) v = mn_nn[j];
+            else if (j < 2 * m) v = mn_no[j - m];
+            else v = mn_on[j - 2 * m];
+            out[j] = v;
         }
-        if (tid >= 32 && tid - 32 < q) {
-            const int j = tid - 32;
-            emit_candidate(G, D.k, D.B, ids[mpad + j], mn_on[j], &c_cand, &c_app, &c_ovf);
-        }
-        __syncthreads();
         if (tid == 0) {
-            atomicAdd(&stats->joins, 1ull);
-            atomicAdd(&stats->sum_m, static_cast<unsigned long long>(m));
-            atomicAdd(&stats->sum_q, static_cast<unsigned long long>(q));
-            atomicAdd(&stats->rows, static_cast<unsigned long long>(m + q));
+            ++my_joins;
+            my_m += static_cast<unsigned long long>(m);
+            my_q += static_cast<unsigned long long>(q);
             atomicAdd(&stats->dist_evals, static_cast<unsigned long long>(c_pairs));
-            atomicAdd(&stats->candidates, static_cast<unsigned long long>(c_cand));
-            atomicAdd(&stats->appended, static_cast<unsigned long long>(c_app));
-            if (c_ovf) atomicAdd(&stats->overflow, static_cast<unsigned long long>(c_ovf));
         }
+    }
+    if (tid == 0 && my_joins) {
+        atomicAdd(&stats->joins, my_joins);
+        atomicAdd(&stats->sum_m, my_m);
+        atomicAdd(&stats->sum_q, my_q);
+        atomicAdd(&stats->rows, my_m + my_q);
+    }
+}
+
+// File the join outputs into the targets' buckets.  Slot j of node x: its
+// target is G_new(x)[j] (j < 2m, as c_nn / c_no of that NEW sample) or
+// G_old(x)[j - 2m].
+__global__ void k_cand_scatter(Dims D, Graph G, Samples S, DevStats* __restrict__ stats) {
+    __shared__ unsigned int c_cand, c_app;
+    if (threadIdx.x == 0) { c_cand = 0; c_app = 0; }
+    __syncthreads();
+    const int slots = 3 * D.cap;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < D.n * slots) {
+        const int64_t x = i / slots;
+        const int j = static_cast<int>(i - x * slots);
+        const int m = S.gcnt[2 * x], q = S.gcnt[2 * x + 1];
+        if (m > 0 && j < 2 * m + q) {
+            const uint64_t key = S.cand[i];
+            if (key != kSentinel) {  // D15: the (inf, inf) tuple inserts nothing
+                atomicAdd(&c_cand, 1u);
+                const uint32_t t = j < 2 * m
+                    ? S.G[static_cast<size_t>(x) * D.cap + (j < m ? j : j - m)]
+                    : S.G[static_cast<size_t>(D.n) * D.cap + static_cast<size_t>(x) * D.cap + (j - 2 * m)];
+                if (key < G.kth[t]) {  // else it cannot enter G[t] (exact, D17)
+                    atomicAdd(&c_app, 1u);
+                    const uint32_t slot = atomicAdd(G.bcnt + t, 1u);
+                    G.bucket[G.boff[t] + slot] = key;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (c_cand) atomicAdd(&stats->candidates, static_cast<unsigned long long>(c_cand));
+        if (c_app) atomicAdd(&stats->appended, static_cast<unsigned long long>(c_app));
     }
 }
 

@@ -41,11 +41,10 @@ constexpr int kMaxIters = 256;
 
 // ---------------------------------------------------------------- layout
 struct Layout {
-    size_t keys, newmask, kth, lock, bcnt, bucket, fwd, fcnt, rcnt, roff, rsrc, G, gcnt, bsum, stats,
+    size_t keys, newmask, kth, bcnt, bucket, fwd, fcnt, rcnt, rcur, off, rsrc, G, gcnt, bsum, cand, stats,
         xnorm, reserved, flag, total;
 };
 
-int bucket_cap(int k) { return k <= 16 ? 32 : 64; }
 int64_t scan_blocks(int64_t n) { return (n + kScanBlock - 1) / kScanBlock; }
 
 size_t align_up(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
@@ -58,21 +57,23 @@ Layout make_layout(int64_t n, int d, int k, int p, bool cosine, bool own_keys, b
         off += align_up(bytes);
         return at;
     };
-    const int cap = 2 * p, B = bucket_cap(k);
+    const int cap = 2 * p;
     L.keys = own_keys ? take(static_cast<size_t>(n) * k * 8) : 0;
     L.newmask = take(static_cast<size_t>(n) * 4);
     L.kth = take(static_cast<size_t>(n) * 8);
-    L.lock = take(static_cast<size_t>(n) * 4);
     L.bcnt = take(static_cast<size_t>(n) * 4);
-    L.bucket = take(static_cast<size_t>(n) * B * 8);
+    // bucket capacity: sum_t [2 (|R_new(t)| + |F_new(t)|) + |R_old(t)| + |F_old(t)|] <= 6 n p
+    L.bucket = take(static_cast<size_t>(6) * n * p * 8);
     L.fwd = take(static_cast<size_t>(2) * n * p * 4);
     L.fcnt = take(static_cast<size_t>(n) * 2);
     L.rcnt = take(static_cast<size_t>(2) * n * 4);
-    L.roff = take(static_cast<size_t>(2) * (n + 1) * 4);
+    L.rcur = take(static_cast<size_t>(2) * n * 4);
+    L.off = take(static_cast<size_t>(3) * (n + 1) * 8);
     L.rsrc = take(static_cast<size_t>(2) * n * p * 4);
     L.G = take(static_cast<size_t>(2) * n * cap * 4);
     L.gcnt = take(static_cast<size_t>(n) * 2);
-    L.bsum = take(static_cast<size_t>(2) * scan_blocks(n) * 4);
+    L.bsum = take(static_cast<size_t>(3) * scan_blocks(n) * 8);
+    L.cand = take(static_cast<size_t>(n) * 3 * cap * 8);
     L.stats = take(sizeof(DevStats) * kMaxIters);
     L.xnorm = cosine ? take(static_cast<size_t>(n) * d * 4) : 0;
     L.reserved = merge ? take(static_cast<size_t>(n) * (k / 2 > 0 ? k / 2 : 1) * 8) : 0;
@@ -194,17 +195,19 @@ struct Run {
         G.keys = keys ? keys : reinterpret_cast<uint64_t*>(ws + L.keys);
         G.newmask = reinterpret_cast<uint32_t*>(ws + L.newmask);
         G.kth = reinterpret_cast<uint64_t*>(ws + L.kth);
-        G.lock = reinterpret_cast<uint32_t*>(ws + L.lock);
         G.bcnt = reinterpret_cast<uint32_t*>(ws + L.bcnt);
         G.bucket = reinterpret_cast<uint64_t*>(ws + L.bucket);
         S.fwd = reinterpret_cast<uint32_t*>(ws + L.fwd);
         S.fcnt = reinterpret_cast<uint8_t*>(ws + L.fcnt);
         S.rcnt = reinterpret_cast<uint32_t*>(ws + L.rcnt);
-        S.roff = reinterpret_cast<uint32_t*>(ws + L.roff);
+        S.rcur = reinterpret_cast<uint32_t*>(ws + L.rcur);
+        S.off = reinterpret_cast<uint64_t*>(ws + L.off);
         S.rsrc = reinterpret_cast<uint32_t*>(ws + L.rsrc);
         S.G = reinterpret_cast<uint32_t*>(ws + L.G);
         S.gcnt = reinterpret_cast<uint8_t*>(ws + L.gcnt);
-        S.bsum = reinterpret_cast<uint32_t*>(ws + L.bsum);
+        S.bsum = reinterpret_cast<uint64_t*>(ws + L.bsum);
+        S.cand = reinterpret_cast<uint64_t*>(ws + L.cand);
+        G.boff = S.off + 2 * (D.n + 1);
         stats = reinterpret_cast<DevStats*>(ws + L.stats);
         Xn = metric == KNNG_COSINE ? reinterpret_cast<const float*>(ws + L.xnorm) : nullptr;
     }
@@ -215,9 +218,9 @@ struct Run {
 
     bool zero_state() {
         if (c.err != cudaSuccess) return false;
-        cudaMemsetAsync(G.lock, 0, static_cast<size_t>(D.n) * 4, c.stream);
         cudaMemsetAsync(G.bcnt, 0, static_cast<size_t>(D.n) * 4, c.stream);
         cudaMemsetAsync(S.rcnt, 0, static_cast<size_t>(2) * D.n * 4, c.stream);
+        cudaMemsetAsync(S.rcur, 0, static_cast<size_t>(2) * D.n * 4, c.stream);
         cudaMemsetAsync(stats, 0, sizeof(DevStats) * kMaxIters, c.stream);
         return true;
     }
@@ -256,22 +259,24 @@ struct Run {
         });
     }
 
-    void merge_sample(int do_merge, int do_sample) {
+    // prev_iter: index of the iteration whose buckets are merged (-1: none)
+    void merge_sample(int do_merge, int do_sample, int prev_iter) {
         const int wpb = 8;
         const int grid = warps_grid(D.n, wpb);
+        DevStats* ps = prev_iter >= 0 ? stats + prev_iter : nullptr;
         c.launch(do_sample ? "k_merge_sample" : "k_merge", [&] {
-            k_merge_sample<<<grid, wpb * 32, wpb * 32 * sizeof(Elem), c.stream>>>(D, G, S, do_merge, do_sample);
+            k_merge_sample<<<grid, wpb * 32, wpb * 32 * sizeof(Elem), c.stream>>>(D, G, S, do_merge, do_sample, ps);
         });
     }
 
     void reverse(uint32_t tword) {
         const int64_t nb = scan_blocks(D.n);
         c.launch("k_scan_reduce", [&] {
-            k_scan_reduce<<<dim3(static_cast<unsigned>(nb), 2), kScanBlock, 0, c.stream>>>(S.rcnt, D.n, S.bsum, nb);
+            k_scan_reduce<<<dim3(static_cast<unsigned>(nb), 3), kScanBlock, 0, c.stream>>>(S, D.n, nb);
         });
-        c.launch("k_scan_bsums", [&] { k_scan_bsums<<<2, kScanBlock, 0, c.stream>>>(S.bsum, nb); });
+        c.launch("k_scan_bsums", [&] { k_scan_bsums<<<3, kScanBlock, 0, c.stream>>>(S.bsum, nb); });
         c.launch("k_scan_final", [&] {
-            k_scan_final<<<dim3(static_cast<unsigned>(nb), 2), kScanBlock, 0, c.stream>>>(S.rcnt, D.n, S.bsum, nb, S.roff);
+            k_scan_final<<<dim3(static_cast<unsigned>(nb), 3), kScanBlock, 0, c.stream>>>(S, D.n, nb);
         });
         const int64_t items = D.n * D.p;
         c.launch("k_rev_scatter", [&] {
@@ -291,18 +296,27 @@ struct Run {
         const int al = ((static_cast<size_t>(D.d) * esz) % 16 == 0 && base % 16 == 0) ? 1 : 0;
         c.launch("k_join", [&] {
             if (metric == KNNG_COSINE)
-                k_join<float, true><<<grid, kJoinThreads, 0, c.stream>>>(nullptr, Xn, D, G, S, boundary, al, st);
+                k_join<float, true><<<grid, kJoinThreads, 0, c.stream>>>(nullptr, Xn, D, S, boundary, al, st);
             else if (dt == KNNG_F32)
-                k_join<float, false><<<grid, kJoinThreads, 0, c.stream>>>(static_cast<const float*>(X), nullptr, D, G, S, boundary, al, st);
+                k_join<float, false><<<grid, kJoinThreads, 0, c.stream>>>(static_cast<const float*>(X), nullptr, D, S, boundary, al, st);
             else
-                k_join<uint8_t, false><<<grid, kJoinThreads, 0, c.stream>>>(static_cast<const uint8_t*>(X), nullptr, D, G, S, boundary, al, st);
+                k_join<uint8_t, false><<<grid, kJoinThreads, 0, c.stream>>>(static_cast<const uint8_t*>(X), nullptr, D, S, boundary, al, st);
+        });
+    }
+
+    void scatter(int iter) {
+        const int64_t items = D.n * 3 * D.cap;
+        DevStats* st = stats + iter;
+        c.launch("k_cand_scatter", [&] {
+            k_cand_scatter<<<static_cast<int>((items + 255) / 256), 256, 0, c.stream>>>(D, G, S, st);
         });
     }
 
     void iteration(int iter, uint32_t tword, bool merge_first) {
-        merge_sample(merge_first ? 1 : 0, 1);
+        merge_sample(merge_first ? 1 : 0, 1, merge_first ? iter - 1 : -1);
         reverse(tword);
         join(iter);
+        scatter(iter);
     }
 
     void export_graph(uint32_t* ids, float* dists) {
@@ -327,7 +341,7 @@ struct Run {
             s.dist_evals = static_cast<int64_t>(h[i].dist_evals);
             s.candidates = static_cast<int64_t>(h[i].candidates);
             s.appended = static_cast<int64_t>(h[i].appended);
-            s.overflow = static_cast<int64_t>(h[i].overflow);
+            s.accepted = static_cast<int64_t>(h[i].accepted);
             s.rows = static_cast<int64_t>(h[i].rows);
             g_last_stats.push_back(s);
         }
@@ -379,7 +393,7 @@ knng_status knng_build(const void* vectors, knng_dtype dt, int64_t n, int32_t d,
     R.L = make_layout(n, d, k, sample_size, metric == KNNG_COSINE, true, false);
     char* ws = nullptr;
     if ((s = get_workspace(c, workspace, workspace_bytes, R.L.total, &ws))) return s;
-    R.D = Dims{n, d, k, sample_size, 2 * sample_size, bucket_cap(k)};
+    R.D = Dims{n, d, k, sample_size, 2 * sample_size};
     R.X = vectors;
     R.dt = dt;
     R.metric = metric;
@@ -389,7 +403,7 @@ knng_status knng_build(const void* vectors, knng_dtype dt, int64_t n, int32_t d,
     if ((s = R.normalize())) return s;
     R.init();
     for (int t = 0; t < iters; ++t) R.iteration(t, static_cast<uint32_t>(t), t > 0);
-    R.merge_sample(1, 0);
+    R.merge_sample(1, 0, iters - 1);
     R.export_graph(out_ids, out_dists);
     R.collect_stats(iters);
     return c.finish();
@@ -511,7 +525,7 @@ knng_status knng_debug_init(const void* vectors, knng_dtype dt, int64_t n, int32
     R.L = make_layout(n, d, k, 1, metric == KNNG_COSINE, false, false);
     char* ws = nullptr;
     if ((s = get_workspace(c, nullptr, 0, R.L.total, &ws))) return s;
-    R.D = Dims{n, d, k, 1, 2, bucket_cap(k)};
+    R.D = Dims{n, d, k, 1, 2};
     R.X = vectors;
     R.dt = dt;
     R.metric = metric;
@@ -540,7 +554,7 @@ knng_status knng_debug_iterate(const void* vectors, knng_dtype dt, int64_t n, in
     R.L = make_layout(n, d, k, sample_size, metric == KNNG_COSINE, false, false);
     char* ws = nullptr;
     if ((s = get_workspace(c, workspace, workspace_bytes, R.L.total, &ws))) return s;
-    R.D = Dims{n, d, k, sample_size, 2 * sample_size, bucket_cap(k)};
+    R.D = Dims{n, d, k, sample_size, 2 * sample_size};
     R.X = vectors;
     R.dt = dt;
     R.metric = metric;
@@ -553,7 +567,7 @@ knng_status knng_debug_iterate(const void* vectors, knng_dtype dt, int64_t n, in
         k_state_in<<<R.warps_grid(n, 8), 256, 0, c.stream>>>(R.D, R.G, flags);
     });
     R.iteration(0, tword, false);
-    R.merge_sample(1, 0);
+    R.merge_sample(1, 0, 0);
     c.launch("k_state_out", [&] {
         k_state_out<<<static_cast<int>((n * k + 255) / 256), 256, 0, c.stream>>>(R.D, R.G, flags);
     });
@@ -576,7 +590,7 @@ knng_status knng_debug_sample(int64_t n, int32_t k, int32_t sample_size, uint32_
     R.L = make_layout(n, 1, k, sample_size, false, true, false);
     char* ws = nullptr;
     if ((s = get_workspace(c, workspace, workspace_bytes, R.L.total, &ws))) return s;
-    R.D = Dims{n, 1, k, sample_size, 2 * sample_size, bucket_cap(k)};
+    R.D = Dims{n, 1, k, sample_size, 2 * sample_size};
     R.metric = KNNG_L2SQ;
     R.seed = seed;
     R.bind(ws, nullptr);
@@ -585,7 +599,7 @@ knng_status knng_debug_sample(int64_t n, int32_t k, int32_t sample_size, uint32_
     c.launch("k_state_in", [&] {
         k_state_in<<<R.warps_grid(n, 8), 256, 0, c.stream>>>(R.D, R.G, flags);
     });
-    R.merge_sample(0, 1);
+    R.merge_sample(0, 1, -1);
     R.reverse(tword);
     c.launch("k_samples_out", [&] {
         k_samples_out<<<static_cast<int>((n * R.D.cap + 255) / 256), 256, 0, c.stream>>>(R.D, R.S, Gn, cn, Go, co);
@@ -645,7 +659,7 @@ knng_status knng_merge(const void* vecA, int64_t nA, const uint32_t* idsA, const
     cudaMemcpyAsync(X, vecA, static_cast<size_t>(nA) * d * esz, cudaMemcpyDeviceToDevice, c.stream);
     cudaMemcpyAsync(X + static_cast<size_t>(nA) * d * esz, vecB, static_cast<size_t>(nB) * d * esz,
                     cudaMemcpyDeviceToDevice, c.stream);
-    R.D = Dims{n, d, k, sample_size, 2 * sample_size, bucket_cap(k)};
+    R.D = Dims{n, d, k, sample_size, 2 * sample_size};
     R.X = X;
     R.dt = dt;
     R.metric = metric;
@@ -670,7 +684,7 @@ knng_status knng_merge(const void* vecA, int64_t nA, const uint32_t* idsA, const
     });
     for (int t = 0; t < merge_iters; ++t)
         R.iteration(t, 0x80000000u | (static_cast<uint32_t>(level) << 16) | static_cast<uint32_t>(t), t > 0);
-    R.merge_sample(1, 0);
+    R.merge_sample(1, 0, merge_iters - 1);
     c.launch("k_ggm_finalize", [&] {
         k_ggm_finalize<<<grid, 256, 256 / 32 * 32 * sizeof(Elem), c.stream>>>(R.D, R.G, reserved);
     });

@@ -128,6 +128,7 @@ def test_iterations_teacher_forced_bit_exact(K, case):
         assert st["dist_evals"] == ost["dist_evals"]
         assert st["joins"] == ost["joins"] and st["sum_m"] == ost["sum_m"] and st["sum_q"] == ost["sum_q"]
         assert st["candidates"] == ost["candidates"]
+        assert st["accepted"] == ost["accepted"]
 
 
 @pytest.mark.parametrize("case", CASES[:3] + CASES[5:6], ids=lambda c: f"{c[0]}-{c[1]}-{c[5]}-{c[6]}")
