@@ -28,7 +28,7 @@
 
 namespace knng {
 
-constexpr int kJoinThreads = 128;
+constexpr int kJoinNodes = 4;  // nodes per CTA batch
 constexpr int kMaxSlots = 64;  // m <= 32 NEW (padded to 4) + q <= 32 OLD
 
 template <typename T>
@@ -58,19 +58,31 @@ __device__ __forceinline__ bool allowed_pair(int64_t boundary, uint32_t a, uint3
     return boundary < 0 || ((static_cast<int64_t>(a) >= boundary) != (static_cast<int64_t>(b) >= boundary));
 }
 
-template <typename T, bool COS>
-__global__ void __launch_bounds__(kJoinThreads)
+// One CTA handles a batch of NB consecutive nodes per step of a persistent
+// loop; the 4x4 register blocks of all NB tiles form one flat list spread
+// over the CTA's 64 NB threads, so warps stay full even though a single
+// node's tile has only ~35-100 blocks (the one-node-per-CTA layout left
+// ~40% of the FP lanes idle).
+template <typename T, bool COS, int NB>
+__global__ void __launch_bounds__(NB * 64, 2)
 k_join(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Samples S, int64_t boundary,
        int aligned16, DevStats* __restrict__ stats) {
     using Cfg = SlabCfg<T>;
     using E = typename std::conditional<COS, float, T>::type;
+    constexpr bool kFloat = std::is_same<E, float>::value;
+    using Acc = typename std::conditional<kFloat, float, unsigned int>::type;
     constexpr int SD = Cfg::kDims, RS = Cfg::kStride, CE = Cfg::kChunkElems;
-    constexpr int CPR = SD / CE;  // 16-B chunks per row per stage
+    constexpr int CPR = SD / CE;               // 16-B chunks per row per stage
+    constexpr int THREADS = NB * 64;
+    constexpr int TILE = kMaxSlots * RS;       // elements of one node's stage
+    constexpr int ROUNDS = (NB * 100 + THREADS - 1) / THREADS;  // <= 100 blocks per node
     const E* __restrict__ V = COS ? reinterpret_cast<const E*>(Xn) : reinterpret_cast<const E*>(X);
 
-    __shared__ __align__(16) E rows[2][kMaxSlots * RS];
-    __shared__ uint32_t ids[kMaxSlots];
-    __shared__ unsigned long long mn_nn[32], mn_no[32], mn_on[32];
+    extern __shared__ __align__(16) unsigned char join_smem[];
+    E* rows = reinterpret_cast<E*>(join_smem);  // [2][NB][TILE]
+    __shared__ uint32_t ids[NB][kMaxSlots];
+    __shared__ unsigned long long mins[NB][3][32];  // c_nn, c_no (per NEW u), c_on (per OLD w)
+    __shared__ int sm_m[NB], sm_q[NB], blk_pre[NB + 1], chk_pre[NB + 1];
     __shared__ unsigned int c_pairs;
 
     const int tid = threadIdx.x;
@@ -78,70 +90,105 @@ k_join(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Samples S,
     const int nslab = (d + SD - 1) / SD;
     unsigned long long my_joins = 0, my_m = 0, my_q = 0;
 
-    for (int64_t x = blockIdx.x; x < D.n; x += gridDim.x) {
-        const int m = S.gcnt[2 * x], q = S.gcnt[2 * x + 1];
-        if (m == 0) continue;  // no NEW sample: nothing to join (block-uniform)
-        const int mpad = (m + 3) & ~3, qpad = (q + 3) & ~3;
-        const int mg = mpad >> 2, qg = qpad >> 2;
-        const int nslots = mpad + qpad;
-        __syncthreads();  // previous node's shared memory fully consumed
-        if (tid < kMaxSlots) {
-            uint32_t id = 0xFFFFFFFFu;
-            if (tid < m) id = S.G[static_cast<size_t>(x) * cap + tid];
-            else if (tid >= mpad && tid - mpad < q)
-                id = S.G[static_cast<size_t>(D.n) * cap + static_cast<size_t>(x) * cap + (tid - mpad)];
-            ids[tid] = id;
+    for (int64_t b0 = static_cast<int64_t>(blockIdx.x) * NB; b0 < D.n; b0 += static_cast<int64_t>(gridDim.x) * NB) {
+        __syncthreads();  // previous batch fully consumed
+        if (tid < NB) {
+            const int64_t x = b0 + tid;
+            int m = 0, q = 0;
+            if (x < D.n) { m = S.gcnt[2 * x]; q = S.gcnt[2 * x + 1]; }
+            if (m == 0) q = 0;  // no NEW sample: nothing to join
+            sm_m[tid] = m;
+            sm_q[tid] = q;
         }
-        if (tid < 32) {
-            mn_nn[tid] = kSentinel;
-            mn_no[tid] = kSentinel;
-            mn_on[tid] = kSentinel;
-        }
+        for (int i = tid; i < NB * 96; i += THREADS) (&mins[0][0][0])[i] = kSentinel;
         if (tid == 0) c_pairs = 0;
         __syncthreads();
-
-        // block assignment: NN lower-triangular blocks (I >= J), then NO blocks
-        const int nnn = mg * (mg + 1) / 2;
-        const int nb = nnn + mg * qg;
-        int I = 0, J = 0;
-        const bool active = tid < nb;
-        if (active) {
-            if (tid < nnn) {
-                I = static_cast<int>((sqrtf(8.0f * tid + 1.0f) - 1.0f) * 0.5f);
-                while ((I + 1) * (I + 2) / 2 <= tid) ++I;
-                while (I * (I + 1) / 2 > tid) --I;
-                J = tid - I * (I + 1) / 2;
-            } else {
-                const int t2 = tid - nnn;
-                I = t2 / qg;
-                J = mg + t2 % qg;
+        if (tid == 0) {
+            int bp = 0, cp = 0;
+            for (int i = 0; i < NB; ++i) {
+                blk_pre[i] = bp;
+                chk_pre[i] = cp;
+                const int mg = (sm_m[i] + 3) >> 2, qg = (sm_q[i] + 3) >> 2;
+                bp += mg * (mg + 1) / 2 + mg * qg;
+                cp += 4 * (mg + qg) * CPR;
             }
+            blk_pre[NB] = bp;
+            chk_pre[NB] = cp;
         }
-        const bool nn = J < mg;
-        const int rbase = 4 * I;
-        const int cbase = nn ? 4 * J : mpad + 4 * (J - mg);
-        const int aoff = rbase * RS, boff = cbase * RS;
+        for (int i = tid; i < NB * kMaxSlots; i += THREADS) {
+            const int nd = i / kMaxSlots, slot = i - nd * kMaxSlots;
+            const int m = sm_m[nd], q = sm_q[nd], mpad = (m + 3) & ~3;
+            const int64_t x = b0 + nd;
+            uint32_t id = 0xFFFFFFFFu;
+            if (slot < m) id = S.G[static_cast<size_t>(x) * cap + slot];
+            else if (slot >= mpad && slot - mpad < q)
+                id = S.G[static_cast<size_t>(D.n) * cap + static_cast<size_t>(x) * cap + (slot - mpad)];
+            ids[nd][slot] = id;
+        }
+        __syncthreads();
+        const int total_blocks = blk_pre[NB];
+        if (total_blocks == 0) continue;  // block-uniform
+        const int total_chunks = chk_pre[NB];
 
-        float acc[4][4];
-        unsigned int iacc[4][4];
+        // this thread's blocks: (node, row base, col base, NN?) per round
+        int b_node[ROUNDS], b_abase[ROUNDS], b_bbase[ROUNDS], b_rb[ROUNDS], b_cb[ROUNDS];
+        bool b_nn[ROUNDS], b_on[ROUNDS];
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
+        for (int r = 0; r < ROUNDS; ++r) {
+            const int f = tid + r * THREADS;
+            b_on[r] = f < total_blocks;
+            int nd = 0;
+            while (nd + 1 < NB && blk_pre[nd + 1] <= f) ++nd;
+            const int t = f - blk_pre[nd];
+            const int m = sm_m[nd], q = sm_q[nd];
+            const int mpad = (m + 3) & ~3, mg = mpad >> 2, qg = (q + 3) >> 2;
+            const int nnn = mg * (mg + 1) / 2;
+            int I = 0, J = 0;
+            if (b_on[r]) {
+                if (t < nnn) {
+                    I = static_cast<int>((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+                    while ((I + 1) * (I + 2) / 2 <= t) ++I;
+                    while (I * (I + 1) / 2 > t) --I;
+                    J = t - I * (I + 1) / 2;
+                } else {
+                    const int t2 = t - nnn;
+                    I = t2 / qg;
+                    J = mg + t2 % qg;
+                }
+            }
+            b_node[r] = nd;
+            b_nn[r] = J < mg;
+            b_rb[r] = 4 * I;
+            b_cb[r] = b_nn[r] ? 4 * J : mpad + 4 * (J - mg);
+            b_abase[r] = nd * TILE + b_rb[r] * RS;
+            b_bbase[r] = nd * TILE + b_cb[r] * RS;
+        }
+
+        Acc acc[ROUNDS][4][4];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) { acc[r][c] = 0.0f; iacc[r][c] = 0u; }
+        for (int r = 0; r < ROUNDS; ++r)
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[r][i][c] = Acc(0);
 
         auto issue = [&](int slab, int stage) {
             const int d0 = slab * SD;
-            for (int c = tid; c < nslots * CPR; c += kJoinThreads) {
-                const int slot = c / CPR, part = c - slot * CPR;
+            E* base = rows + stage * NB * TILE;
+            for (int c = tid; c < total_chunks; c += THREADS) {
+                int nd = 0;
+                while (nd + 1 < NB && chk_pre[nd + 1] <= c) ++nd;
+                const int cl = c - chk_pre[nd];
+                const int slot = cl / CPR, part = cl - slot * CPR;
                 const int e0 = d0 + part * CE;
-                const uint32_t id = ids[slot];
+                const uint32_t id = ids[nd][slot];
                 int cnt = 0;
                 const E* src = V;
                 if (id != 0xFFFFFFFFu && e0 < d) {
                     cnt = min(CE, d - e0);
                     src = V + static_cast<size_t>(id) * d + e0;
                 }
-                E* dst = &rows[stage][slot * RS + part * CE];
+                E* dst = base + nd * TILE + slot * RS + part * CE;
                 if (aligned16) {
                     cp_async16(dst, src, cnt * static_cast<int>(sizeof(E)));
                 } else {  // rows not 16-B aligned (d * sizeof(E) % 16 != 0)
@@ -161,32 +208,35 @@ k_join(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Samples S,
                 cp_async_wait<0>();
             }
             __syncthreads();
-            if (active) {
-                const E* __restrict__ A = rows[sl & 1] + aoff;
-                const E* __restrict__ B = rows[sl & 1] + boff;
-                if constexpr (std::is_same<E, float>::value) {
+            const E* st = rows + (sl & 1) * NB * TILE;
+#pragma unroll
+            for (int r = 0; r < ROUNDS; ++r) {
+                if (!b_on[r]) continue;
+                const E* __restrict__ A = st + b_abase[r];
+                const E* __restrict__ B = st + b_bbase[r];
+                if constexpr (kFloat) {
 #pragma unroll
                     for (int i = 0; i < SD; i += 4) {
                         float4 a[4], b[4];
 #pragma unroll
-                        for (int r = 0; r < 4; ++r) a[r] = *reinterpret_cast<const float4*>(A + r * RS + i);
+                        for (int rr = 0; rr < 4; ++rr) a[rr] = *reinterpret_cast<const float4*>(A + rr * RS + i);
 #pragma unroll
                         for (int c = 0; c < 4; ++c) b[c] = *reinterpret_cast<const float4*>(B + c * RS + i);
 #pragma unroll
-                        for (int r = 0; r < 4; ++r)
+                        for (int rr = 0; rr < 4; ++rr)
 #pragma unroll
                             for (int c = 0; c < 4; ++c) {
                                 if constexpr (COS) {
-                                    acc[r][c] = fmaf(a[r].x, b[c].x, acc[r][c]);
-                                    acc[r][c] = fmaf(a[r].y, b[c].y, acc[r][c]);
-                                    acc[r][c] = fmaf(a[r].z, b[c].z, acc[r][c]);
-                                    acc[r][c] = fmaf(a[r].w, b[c].w, acc[r][c]);
+                                    acc[r][rr][c] = fmaf(a[rr].x, b[c].x, acc[r][rr][c]);
+                                    acc[r][rr][c] = fmaf(a[rr].y, b[c].y, acc[r][rr][c]);
+                                    acc[r][rr][c] = fmaf(a[rr].z, b[c].z, acc[r][rr][c]);
+                                    acc[r][rr][c] = fmaf(a[rr].w, b[c].w, acc[r][rr][c]);
                                 } else {
                                     float t;
-                                    t = a[r].x - b[c].x; acc[r][c] = fmaf(t, t, acc[r][c]);
-                                    t = a[r].y - b[c].y; acc[r][c] = fmaf(t, t, acc[r][c]);
-                                    t = a[r].z - b[c].z; acc[r][c] = fmaf(t, t, acc[r][c]);
-                                    t = a[r].w - b[c].w; acc[r][c] = fmaf(t, t, acc[r][c]);
+                                    t = a[rr].x - b[c].x; acc[r][rr][c] = fmaf(t, t, acc[r][rr][c]);
+                                    t = a[rr].y - b[c].y; acc[r][rr][c] = fmaf(t, t, acc[r][rr][c]);
+                                    t = a[rr].z - b[c].z; acc[r][rr][c] = fmaf(t, t, acc[r][rr][c]);
+                                    t = a[rr].w - b[c].w; acc[r][rr][c] = fmaf(t, t, acc[r][rr][c]);
                                 }
                             }
                     }
@@ -196,15 +246,15 @@ k_join(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Samples S,
                     for (int i = 0; i < SD; i += 4) {
                         uint32_t a[4], b[4];
 #pragma unroll
-                        for (int r = 0; r < 4; ++r) a[r] = *reinterpret_cast<const uint32_t*>(A + r * RS + i);
+                        for (int rr = 0; rr < 4; ++rr) a[rr] = *reinterpret_cast<const uint32_t*>(A + rr * RS + i);
 #pragma unroll
                         for (int c = 0; c < 4; ++c) b[c] = *reinterpret_cast<const uint32_t*>(B + c * RS + i);
 #pragma unroll
-                        for (int r = 0; r < 4; ++r)
+                        for (int rr = 0; rr < 4; ++rr)
 #pragma unroll
                             for (int c = 0; c < 4; ++c) {
-                                const uint32_t ad = __vabsdiffu4(a[r], b[c]);
-                                iacc[r][c] = __dp4a(ad, ad, iacc[r][c]);
+                                const uint32_t ad = __vabsdiffu4(a[rr], b[c]);
+                                acc[r][rr][c] = __dp4a(ad, ad, acc[r][rr][c]);
                             }
                     }
                 }
@@ -213,31 +263,40 @@ k_join(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Samples S,
         }
 
         // ---- selection (Alg. 2): per-thread pre-reduction + smem atomicMin
-        if (active) {
-            unsigned pairs = 0;
+        unsigned pairs = 0;
+#pragma unroll
+        for (int r = 0; r < ROUNDS; ++r) {
+            if (!b_on[r]) continue;
+            const int nd = b_node[r];
+            const int m = sm_m[nd], q = sm_q[nd], mpad = (m + 3) & ~3;
+            const bool nn = b_nn[r];
+            const uint32_t* nid = ids[nd];
+            unsigned long long* mn_nn = mins[nd][0];
+            unsigned long long* mn_no = mins[nd][1];
+            unsigned long long* mn_on = mins[nd][2];
             uint64_t colbest[4] = {kSentinel, kSentinel, kSentinel, kSentinel};
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const int u = rbase + r;
+            for (int rr = 0; rr < 4; ++rr) {
+                const int u = b_rb[r] + rr;
                 uint64_t rowbest = kSentinel;
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
-                    const int w = cbase + c;
+                    const int w = b_cb[r] + c;
                     bool valid = nn ? (u < m && w < u) : (u < m && (w - mpad) < q);
-                    if (valid) valid = allowed_pair(boundary, ids[u], ids[w]);
+                    if (valid) valid = allowed_pair(boundary, nid[u], nid[w]);
                     if (!valid) continue;
                     float dist;
                     if constexpr (COS) {
-                        const float rr = 1.0f - acc[r][c];
-                        dist = rr > 0.0f ? rr : 0.0f;
-                    } else if constexpr (std::is_same<E, float>::value) {
-                        dist = acc[r][c];
+                        const float x1 = 1.0f - acc[r][rr][c];
+                        dist = x1 > 0.0f ? x1 : 0.0f;
+                    } else if constexpr (kFloat) {
+                        dist = acc[r][rr][c];
                     } else {
-                        dist = static_cast<float>(iacc[r][c]);
+                        dist = static_cast<float>(acc[r][rr][c]);
                     }
                     ++pairs;
-                    const uint64_t kr = make_key(dist, ids[w]);
-                    const uint64_t kc = make_key(dist, ids[u]);
+                    const uint64_t kr = make_key(dist, nid[w]);
+                    const uint64_t kc = make_key(dist, nid[u]);
                     rowbest = kr < rowbest ? kr : rowbest;
                     colbest[c] = kc < colbest[c] ? kc : colbest[c];
                 }
@@ -249,29 +308,33 @@ k_join(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Samples S,
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 if (colbest[c] == kSentinel) continue;
-                const int w = cbase + c;
+                const int w = b_cb[r] + c;
                 if (nn) atomicMin(&mn_nn[w], static_cast<unsigned long long>(colbest[c]));
                 else atomicMin(&mn_on[w - mpad], static_cast<unsigned long long>(colbest[c]));
             }
-            if (pairs) atomicAdd(&c_pairs, pairs);
         }
+        if (pairs) atomicAdd(&c_pairs, pairs);
         __syncthreads();
 
         // ---- output: slot j of node x holds c_nn(u_j) (j < m), c_no(u_j)
         // (m <= j < 2m), c_on(w_j) (2m <= j < 2m + q)  (Alg. 1 lines 12-31)
-        uint64_t* out = S.cand + static_cast<size_t>(x) * (3 * cap);
-        const int total = 2 * m + q;
-        for (int j = tid; j < total; j += kJoinThreads) {
+        for (int i = tid; i < NB * 3 * 32; i += THREADS) {
+            const int nd = i / 96, j = i - nd * 96;
+            const int m = sm_m[nd], q = sm_q[nd];
+            if (j >= 2 * m + q) continue;
             uint64_t v;
-            if (j < m) v = mn_nn[j];
-            else if (j < 2 * m) v = mn_no[j - m];
-            else v = mn_on[j - 2 * m];
-            out[j] = v;
+            if (j < m) v = mins[nd][0][j];
+            else if (j < 2 * m) v = mins[nd][1][j - m];
+            else v = mins[nd][2][j - 2 * m];
+            S.cand[static_cast<size_t>(b0 + nd) * (3 * cap) + j] = v;
         }
         if (tid == 0) {
-            ++my_joins;
-            my_m += static_cast<unsigned long long>(m);
-            my_q += static_cast<unsigned long long>(q);
+            for (int i = 0; i < NB; ++i)
+                if (sm_m[i] > 0) {
+                    ++my_joins;
+                    my_m += static_cast<unsigned long long>(sm_m[i]);
+                    my_q += static_cast<unsigned long long>(sm_q[i]);
+                }
             atomicAdd(&stats->dist_evals, static_cast<unsigned long long>(c_pairs));
         }
     }
@@ -281,6 +344,12 @@ k_join(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Samples S,
         atomicAdd(&stats->sum_q, my_q);
         atomicAdd(&stats->rows, my_m + my_q);
     }
+}
+
+template <typename T, bool COS, int NB>
+constexpr size_t join_smem_bytes() {
+    using E = typename std::conditional<COS, float, T>::type;
+    return sizeof(E) * 2 * NB * kMaxSlots * SlabCfg<T>::kStride;
 }
 
 // File the join outputs into the targets' buckets.  Slot j of node x: its

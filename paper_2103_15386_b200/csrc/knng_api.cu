@@ -289,18 +289,31 @@ struct Run {
     }
 
     void join(int iter) {
-        const int grid = static_cast<int>(D.n < (1 << 20) ? D.n : (1 << 20));
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+        const int64_t batches = (D.n + kJoinNodes - 1) / kJoinNodes;
+        const int grid = static_cast<int>(batches < 8ll * sms ? batches : 8ll * sms);
         DevStats* st = stats + iter;
         const size_t esz = (metric == KNNG_COSINE || dt == KNNG_F32) ? 4 : 1;
         const uintptr_t base = metric == KNNG_COSINE ? reinterpret_cast<uintptr_t>(Xn) : reinterpret_cast<uintptr_t>(X);
         const int al = ((static_cast<size_t>(D.d) * esz) % 16 == 0 && base % 16 == 0) ? 1 : 0;
+        constexpr int NB = kJoinNodes;
         c.launch("k_join", [&] {
-            if (metric == KNNG_COSINE)
-                k_join<float, true><<<grid, kJoinThreads, 0, c.stream>>>(nullptr, Xn, D, S, boundary, al, st);
-            else if (dt == KNNG_F32)
-                k_join<float, false><<<grid, kJoinThreads, 0, c.stream>>>(static_cast<const float*>(X), nullptr, D, S, boundary, al, st);
-            else
-                k_join<uint8_t, false><<<grid, kJoinThreads, 0, c.stream>>>(static_cast<const uint8_t*>(X), nullptr, D, S, boundary, al, st);
+            if (metric == KNNG_COSINE) {
+                constexpr size_t sm = join_smem_bytes<float, true, NB>();
+                cudaFuncSetAttribute(k_join<float, true, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+                k_join<float, true, NB><<<grid, NB * 64, sm, c.stream>>>(nullptr, Xn, D, S, boundary, al, st);
+            } else if (dt == KNNG_F32) {
+                constexpr size_t sm = join_smem_bytes<float, false, NB>();
+                cudaFuncSetAttribute(k_join<float, false, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+                k_join<float, false, NB><<<grid, NB * 64, sm, c.stream>>>(static_cast<const float*>(X), nullptr, D, S,
+                                                                         boundary, al, st);
+            } else {
+                constexpr size_t sm = join_smem_bytes<uint8_t, false, NB>();
+                cudaFuncSetAttribute(k_join<uint8_t, false, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+                k_join<uint8_t, false, NB><<<grid, NB * 64, sm, c.stream>>>(static_cast<const uint8_t*>(X), nullptr, D,
+                                                                           S, boundary, al, st);
+            }
         });
     }
 
