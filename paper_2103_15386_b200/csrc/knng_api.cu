@@ -15,6 +15,7 @@
 #include "eval_kernels.cuh"
 #include "ggm_kernels.cuh"
 #include "join_kernel.cuh"
+#include "join_ws.cuh"
 
 using namespace knng;
 
@@ -298,6 +299,42 @@ struct Run {
         const uintptr_t base = metric == KNNG_COSINE ? reinterpret_cast<uintptr_t>(Xn) : reinterpret_cast<uintptr_t>(X);
         const int al = ((static_cast<size_t>(D.d) * esz) % 16 == 0 && base % 16 == 0) ? 1 : 0;
         constexpr int NB = kJoinNodes;
+        static const bool force_v3 = [] {
+            const char* e = getenv("KNNG_JOIN");
+            return e && strcmp(e, "v3") == 0;
+        }();
+        static const int dbg_mode = [] {
+            const char* e = getenv("KNNG_JOIN_DBG");
+            const int v = e ? atoi(e) : 0;
+            if (v) cudaMemcpyToSymbol(g_join_dbg, &v, sizeof(int));
+            return v;
+        }();
+        (void)dbg_mode;
+        if (al && !force_v3) {
+            // warp-specialised pipeline (bulk row copies need 16-B aligned,
+            // 16-B multiple row slabs)
+            constexpr int STG = 5;
+            unsigned long long* work = reinterpret_cast<unsigned long long*>(ws + L.flag + 8);
+            cudaMemsetAsync(work, 0, 8, c.stream);
+            c.launch("k_join", [&] {
+                if (metric == KNNG_COSINE) {
+                    constexpr size_t sm = WsCfg<float, true, STG>::kSmem;
+                    cudaFuncSetAttribute(k_join_ws<float, true, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+                    k_join_ws<float, true, STG><<<sms, kWsThreads, sm, c.stream>>>(nullptr, Xn, D, S, boundary, work, st);
+                } else if (dt == KNNG_F32) {
+                    constexpr size_t sm = WsCfg<float, false, STG>::kSmem;
+                    cudaFuncSetAttribute(k_join_ws<float, false, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+                    k_join_ws<float, false, STG><<<sms, kWsThreads, sm, c.stream>>>(static_cast<const float*>(X), nullptr, D,
+                                                                                    S, boundary, work, st);
+                } else {
+                    constexpr size_t sm = WsCfg<uint8_t, false, STG>::kSmem;
+                    cudaFuncSetAttribute(k_join_ws<uint8_t, false, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+                    k_join_ws<uint8_t, false, STG><<<sms, kWsThreads, sm, c.stream>>>(static_cast<const uint8_t*>(X), nullptr,
+                                                                                      D, S, boundary, work, st);
+                }
+            });
+            return;
+        }
         c.launch("k_join", [&] {
             if (metric == KNNG_COSINE) {
                 constexpr size_t sm = join_smem_bytes<float, true, NB>();

@@ -40,3 +40,23 @@ for op, (st, ex) in sorted(by_op.items(), key=lambda x: -x[1][1])[:25]:
 print("-- hottest instructions by stall samples")
 for st, ex, idx, src in sorted(inst, reverse=True)[:top]:
     print(f"  {100*st/TS:5.1f}% st {ex:10.3e} ex  #{idx:5d} {src}")
+
+
+def top_by(col, k=12):
+    j = h.index(col)
+    items = []
+    for idx, r in enumerate(rows[1:]):
+        try:
+            items.append((float(r[j] or 0), idx, r[iS].strip()[:80], float(r[iEx] or 0)))
+        except ValueError:
+            pass
+    items.sort(reverse=True)
+    tot = sum(x[0] for x in items) or 1
+    print(f"-- top by {col} (total {tot:.0f})")
+    for v, idx, src, ex in items[:k]:
+        print(f"  {100*v/tot:5.1f}%  #{idx:5d} ex {ex:10.3e}  {src}")
+
+
+if len(sys.argv) > 3:
+    for c in sys.argv[3].split(","):
+        top_by(c)
