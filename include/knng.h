@@ -170,6 +170,24 @@ knng_status knng_debug_philox(const uint32_t* ctr, int64_t m, uint64_t seed,
                               uint32_t* out, void* stream);
 
 /* ------------------------------------------------------------------------
+ * Options (process-wide; names are case-sensitive; unknown name ->
+ * KNNG_E_USAGE).
+ *   "exact_u8"     1 (default): float32 input under KNNG_L2SQ whose values
+ *                  are all integers in [0, 255] and d <= 258 (so every
+ *                  distance is an exact integer < 2^24) is copied once to
+ *                  uint8 and built on the integer path.  Every distance is
+ *                  then the same exact integer the canonical fp32 evaluation
+ *                  (D5) yields, so the graph is bit-identical; SIFT-like data
+ *                  qualifies.  0: always use the float path.
+ *   "join_kernel"  0 (default): warp-specialised join (join_ws.cuh);
+ *                  1: the batched cp.async join (join_kernel.cuh).
+ *   "last_exact_u8" (read-only) 1 if the last build/merge on this thread ran
+ *                  on the exact integer path.
+ * ---------------------------------------------------------------------- */
+knng_status knng_set_option(const char* name, int64_t value);
+knng_status knng_get_option(const char* name, int64_t* host_value);
+
+/* ------------------------------------------------------------------------
  * Introspection
  * ---------------------------------------------------------------------- */
 /* Counters of the iterations of the last build/merge on this thread (host):

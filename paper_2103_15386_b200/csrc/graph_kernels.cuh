@@ -406,6 +406,23 @@ __global__ void k_normalize(const float* __restrict__ X, int64_t n, int d, float
     for (int j = 0; j < d; ++j) y[j] = x[j] * r;
 }
 
+// option exact_u8: flag any value that is not an integer in [0, 255]
+__global__ void k_check_u8(const float* __restrict__ X, int64_t total, int* bad) {
+    bool ok = true;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const float v = X[i];
+        ok &= (v >= 0.0f && v <= 255.0f && v == rintf(v));
+    }
+    if (__syncthreads_or(!ok) && threadIdx.x == 0) atomicExch(bad, 1);
+}
+
+__global__ void k_to_u8(const float* __restrict__ X, int64_t total, uint8_t* __restrict__ Y) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        Y[i] = static_cast<uint8_t>(X[i]);
+}
+
 __global__ void k_philox_test(const uint32_t* __restrict__ ctr, int64_t m, uint64_t seed, uint32_t* out) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= m) return;

@@ -41,8 +41,8 @@ struct SlabCfg<float> {
 };
 template <>
 struct SlabCfg<uint8_t> {
-    static constexpr int kDims = 32;
-    static constexpr int kStride = 48;
+    static constexpr int kDims = 128;         // 128-B row slab, like f32
+    static constexpr int kStride = 144;
     static constexpr int kChunkElems = 16;
 };
 

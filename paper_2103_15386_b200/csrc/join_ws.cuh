@@ -100,12 +100,13 @@ template <typename T, bool COS, int STAGES>
 struct WsCfg {
     using E = typename std::conditional<COS, float, T>::type;
     static constexpr int SD = SlabCfg<T>::kDims;
-    // float rows: 128-B rows whose 16-B chunks are XOR-swizzled by
-    // (slot >> 2) & 7, so the LDS.128 of lanes on different 4-row groups
-    // never share a bank group (padding cannot: rows 4 apart always collide);
-    // u8: padded rows.
-    static constexpr bool kSwz = std::is_same<E, float>::value;
-    static constexpr int RS = kSwz ? SD : SlabCfg<T>::kStride;
+    // 128-B row slabs (32 f32 or 128 u8 dims) whose 16-B chunks are
+    // XOR-swizzled by (slot >> 2) & 7, so the LDS.128 of lanes on different
+    // 4-row groups never share a bank group (padding cannot: rows 4 apart
+    // always collide).
+    static constexpr bool kSwz = true;
+    static constexpr int RS = SD;
+    static_assert(SD * sizeof(E) == 128, "row slabs are 128 B");
     static constexpr size_t kStageBytes = sizeof(E) * kWsSlots * RS;
     static constexpr size_t kMetaOff = kStageBytes * STAGES;
     static constexpr size_t kPartOff = (kMetaOff + sizeof(WsMeta) * kWsMeta + 15) & ~size_t(15);
@@ -464,20 +465,25 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Samples
                             }
                     }
                 } else {
+                    // uint8: exact integer sum of squares (D5); one LDS.128
+                    // per row brings 16 dims, 2 instructions per 4 dims/pair
+#pragma unroll 2
+                    for (int j = 0; j < SD / 16; ++j) {
+                        if (j * 16 >= lim) break;
+                        uint4 a[4], bv[4];
 #pragma unroll
-                    for (int i = 0; i < SD; i += 4) {
-                        if (i >= lim) break;
-                        uint32_t a[4], bv[4];
+                        for (int r = 0; r < 4; ++r) a[r] = *reinterpret_cast<const uint4*>(A + r * RS + ((j ^ fA) << 4));
 #pragma unroll
-                        for (int r = 0; r < 4; ++r) a[r] = *reinterpret_cast<const uint32_t*>(A + r * RS + i);
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) bv[c] = *reinterpret_cast<const uint32_t*>(B + c * RS + i);
+                        for (int c = 0; c < 4; ++c) bv[c] = *reinterpret_cast<const uint4*>(B + c * RS + ((j ^ fB) << 4));
 #pragma unroll
                         for (int r = 0; r < 4; ++r)
 #pragma unroll
                             for (int c = 0; c < 4; ++c) {
-                                const uint32_t ad = __vabsdiffu4(a[r], bv[c]);
-                                acc[r][c] = __dp4a(ad, ad, acc[r][c]);
+                                uint32_t ad;
+                                ad = __vabsdiffu4(a[r].x, bv[c].x); acc[r][c] = __dp4a(ad, ad, acc[r][c]);
+                                ad = __vabsdiffu4(a[r].y, bv[c].y); acc[r][c] = __dp4a(ad, ad, acc[r][c]);
+                                ad = __vabsdiffu4(a[r].z, bv[c].z); acc[r][c] = __dp4a(ad, ad, acc[r][c]);
+                                ad = __vabsdiffu4(a[r].w, bv[c].w); acc[r][c] = __dp4a(ad, ad, acc[r][c]);
                             }
                     }
                 }

@@ -25,6 +25,9 @@ thread_local std::string g_err;
 thread_local std::vector<knng_iter_stats> g_last_stats;
 std::atomic<int64_t> g_launches{0};
 std::atomic<int> g_timing{0};
+std::atomic<int> g_opt_exact_u8{1};
+std::atomic<int> g_opt_join_kernel{0};
+thread_local int g_last_exact_u8 = 0;
 std::mutex g_time_mu;
 std::map<std::string, std::pair<double, int64_t>> g_times;
 
@@ -43,14 +46,14 @@ constexpr int kMaxIters = 256;
 // ---------------------------------------------------------------- layout
 struct Layout {
     size_t keys, newmask, kth, bcnt, bucket, fwd, fcnt, rcnt, rcur, off, rsrc, G, gcnt, bsum, cand, stats,
-        xnorm, reserved, flag, total;
+        xnorm, xu8, reserved, flag, total;
 };
 
 int64_t scan_blocks(int64_t n) { return (n + kScanBlock - 1) / kScanBlock; }
 
 size_t align_up(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
-Layout make_layout(int64_t n, int d, int k, int p, bool cosine, bool own_keys, bool merge) {
+Layout make_layout(int64_t n, int d, int k, int p, bool cosine, bool own_keys, bool merge, bool u8copy = false) {
     Layout L{};
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -78,6 +81,7 @@ Layout make_layout(int64_t n, int d, int k, int p, bool cosine, bool own_keys, b
     L.stats = take(sizeof(DevStats) * kMaxIters);
     L.xnorm = cosine ? take(static_cast<size_t>(n) * d * 4) : 0;
     L.reserved = merge ? take(static_cast<size_t>(n) * (k / 2 > 0 ? k / 2 : 1) * 8) : 0;
+    L.xu8 = u8copy ? take(static_cast<size_t>(n) * d) : 0;  // exact integer copy (option exact_u8)
     L.flag = take(16);
     L.total = off;
     return L;
@@ -247,6 +251,34 @@ struct Run {
         return KNNG_OK;
     }
 
+    // Option exact_u8: float32 L2 input whose values are all integers in
+    // [0, 255] with d <= 258 is built on an exact uint8 copy.  Every squared
+    // difference and every partial sum is then an integer < 2^24, so the
+    // canonical fp32 accumulation (D5) is exact and equals the integer sum:
+    // the graph is bit-identical, with a quarter of the gather bytes.
+    void compress() {
+        g_last_exact_u8 = 0;
+        if (!(metric == KNNG_L2SQ && dt == KNNG_F32 && L.xu8 && D.d <= 258 && g_opt_exact_u8.load()))
+            return;
+        if (c.err != cudaSuccess) return;
+        int* flag = reinterpret_cast<int*>(ws + L.flag);
+        const int64_t total = D.n * D.d;
+        cudaMemsetAsync(flag, 0, 4, c.stream);
+        c.launch("k_check_u8", [&] {
+            k_check_u8<<<4 * 148, 256, 0, c.stream>>>(static_cast<const float*>(X), total, flag);
+        });
+        int h = 1;
+        cudaMemcpyAsync(&h, flag, 4, cudaMemcpyDeviceToHost, c.stream);
+        if (cudaStreamSynchronize(c.stream) != cudaSuccess || h) return;
+        uint8_t* xu8 = reinterpret_cast<uint8_t*>(ws + L.xu8);
+        c.launch("k_to_u8", [&] {
+            k_to_u8<<<4 * 148, 256, 0, c.stream>>>(static_cast<const float*>(X), total, xu8);
+        });
+        X = xu8;
+        dt = KNNG_U8;
+        g_last_exact_u8 = 1;
+    }
+
     void init() {
         const int wpb = 8;
         const int grid = warps_grid(D.n, wpb);
@@ -299,10 +331,7 @@ struct Run {
         const uintptr_t base = metric == KNNG_COSINE ? reinterpret_cast<uintptr_t>(Xn) : reinterpret_cast<uintptr_t>(X);
         const int al = ((static_cast<size_t>(D.d) * esz) % 16 == 0 && base % 16 == 0) ? 1 : 0;
         constexpr int NB = kJoinNodes;
-        static const bool force_v3 = [] {
-            const char* e = getenv("KNNG_JOIN");
-            return e && strcmp(e, "v3") == 0;
-        }();
+        const bool force_v3 = g_opt_join_kernel.load() == 1;
         static const int dbg_mode = [] {
             const char* e = getenv("KNNG_JOIN_DBG");
             const int v = e ? atoi(e) : 0;
@@ -424,7 +453,7 @@ extern "C" {
 size_t knng_build_workspace_bytes(knng_dtype dt, int64_t n, int32_t d, int32_t k, int32_t sample_size,
                                   knng_metric metric) {
     if (check_common(dt, n, d, k, metric, sample_size) != KNNG_OK) return 0;
-    return make_layout(n, d, k, sample_size, metric == KNNG_COSINE, true, false).total;
+    return make_layout(n, d, k, sample_size, metric == KNNG_COSINE, true, false, dt == KNNG_F32 && metric == KNNG_L2SQ).total;
 }
 
 knng_status knng_build(const void* vectors, knng_dtype dt, int64_t n, int32_t d, int32_t k, knng_metric metric,
@@ -440,7 +469,7 @@ knng_status knng_build(const void* vectors, knng_dtype dt, int64_t n, int32_t d,
     c.stream = static_cast<cudaStream_t>(stream);
     c.timing = g_timing.load() != 0;
     Run R(c);
-    R.L = make_layout(n, d, k, sample_size, metric == KNNG_COSINE, true, false);
+    R.L = make_layout(n, d, k, sample_size, metric == KNNG_COSINE, true, false, dt == KNNG_F32 && metric == KNNG_L2SQ);
     char* ws = nullptr;
     if ((s = get_workspace(c, workspace, workspace_bytes, R.L.total, &ws))) return s;
     R.D = Dims{n, d, k, sample_size, 2 * sample_size};
@@ -451,6 +480,7 @@ knng_status knng_build(const void* vectors, knng_dtype dt, int64_t n, int32_t d,
     R.bind(ws, nullptr);
     R.zero_state();
     if ((s = R.normalize())) return s;
+    R.compress();
     R.init();
     for (int t = 0; t < iters; ++t) R.iteration(t, static_cast<uint32_t>(t), t > 0);
     R.merge_sample(1, 0, iters - 1);
@@ -572,7 +602,7 @@ knng_status knng_debug_init(const void* vectors, knng_dtype dt, int64_t n, int32
     c.stream = static_cast<cudaStream_t>(stream);
     c.timing = g_timing.load() != 0;
     Run R(c);
-    R.L = make_layout(n, d, k, 1, metric == KNNG_COSINE, false, false);
+    R.L = make_layout(n, d, k, 1, metric == KNNG_COSINE, false, false, dt == KNNG_F32 && metric == KNNG_L2SQ);
     char* ws = nullptr;
     if ((s = get_workspace(c, nullptr, 0, R.L.total, &ws))) return s;
     R.D = Dims{n, d, k, 1, 2};
@@ -582,6 +612,7 @@ knng_status knng_debug_init(const void* vectors, knng_dtype dt, int64_t n, int32
     R.seed = seed;
     R.bind(ws, keys);
     if ((s = R.normalize())) return s;
+    R.compress();
     R.init();
     c.launch("k_state_out", [&] {
         k_state_out<<<static_cast<int>((n * k + 255) / 256), 256, 0, c.stream>>>(R.D, R.G, flags);
@@ -601,7 +632,7 @@ knng_status knng_debug_iterate(const void* vectors, knng_dtype dt, int64_t n, in
     c.stream = static_cast<cudaStream_t>(stream);
     c.timing = g_timing.load() != 0;
     Run R(c);
-    R.L = make_layout(n, d, k, sample_size, metric == KNNG_COSINE, false, false);
+    R.L = make_layout(n, d, k, sample_size, metric == KNNG_COSINE, false, false, dt == KNNG_F32 && metric == KNNG_L2SQ);
     char* ws = nullptr;
     if ((s = get_workspace(c, workspace, workspace_bytes, R.L.total, &ws))) return s;
     R.D = Dims{n, d, k, sample_size, 2 * sample_size};
@@ -613,6 +644,7 @@ knng_status knng_debug_iterate(const void* vectors, knng_dtype dt, int64_t n, in
     R.bind(ws, keys);
     R.zero_state();
     if ((s = R.normalize())) return s;
+    R.compress();
     c.launch("k_state_in", [&] {
         k_state_in<<<R.warps_grid(n, 8), 256, 0, c.stream>>>(R.D, R.G, flags);
     });
@@ -675,7 +707,7 @@ size_t knng_merge_workspace_bytes(knng_dtype dt, int64_t nA, int64_t nB, int32_t
     if (check_common(dt, nA + nB, d, k, metric, sample_size) != KNNG_OK) return 0;
     const int64_t n = nA + nB;
     const size_t vbytes = static_cast<size_t>(n) * d * (dt == KNNG_F32 ? 4 : 1);
-    return make_layout(n, d, k, sample_size, metric == KNNG_COSINE, true, true).total + align_up(vbytes);
+    return make_layout(n, d, k, sample_size, metric == KNNG_COSINE, true, true, dt == KNNG_F32 && metric == KNNG_L2SQ).total + align_up(vbytes);
 }
 
 knng_status knng_merge(const void* vecA, int64_t nA, const uint32_t* idsA, const float* distsA, const void* vecB,
@@ -699,7 +731,7 @@ knng_status knng_merge(const void* vecA, int64_t nA, const uint32_t* idsA, const
     c.stream = static_cast<cudaStream_t>(stream);
     c.timing = g_timing.load() != 0;
     Run R(c);
-    R.L = make_layout(n, d, k, sample_size, metric == KNNG_COSINE, true, true);
+    R.L = make_layout(n, d, k, sample_size, metric == KNNG_COSINE, true, true, dt == KNNG_F32 && metric == KNNG_L2SQ);
     const size_t esz = dt == KNNG_F32 ? 4 : 1;
     const size_t vbytes = static_cast<size_t>(n) * d * esz;
     char* ws = nullptr;
@@ -718,17 +750,18 @@ knng_status knng_merge(const void* vecA, int64_t nA, const uint32_t* idsA, const
     R.bind(ws, nullptr);
     R.zero_state();
     if ((s = R.normalize())) return s;
+    R.compress();
     uint64_t* reserved = reinterpret_cast<uint64_t*>(ws + R.L.reserved);
     const int grid = R.warps_grid(n, 8);
     c.launch("k_ggm_seed", [&] {
         if (metric == KNNG_COSINE)
             k_ggm_seed<float, true><<<grid, 256, 0, c.stream>>>(nullptr, R.Xn, R.D, nA, level, seed, idsA, distsA, idsB,
                                                                 distsB, R.G, reserved);
-        else if (dt == KNNG_F32)
-            k_ggm_seed<float, false><<<grid, 256, 0, c.stream>>>(reinterpret_cast<const float*>(X), nullptr, R.D, nA,
+        else if (R.dt == KNNG_F32)
+            k_ggm_seed<float, false><<<grid, 256, 0, c.stream>>>(reinterpret_cast<const float*>(R.X), nullptr, R.D, nA,
                                                                  level, seed, idsA, distsA, idsB, distsB, R.G, reserved);
         else
-            k_ggm_seed<uint8_t, false><<<grid, 256, 0, c.stream>>>(reinterpret_cast<const uint8_t*>(X), nullptr, R.D,
+            k_ggm_seed<uint8_t, false><<<grid, 256, 0, c.stream>>>(reinterpret_cast<const uint8_t*>(R.X), nullptr, R.D,
                                                                    nA, level, seed, idsA, distsA, idsB, distsB, R.G,
                                                                    reserved);
     });
@@ -785,6 +818,29 @@ const char* knng_status_string(knng_status s) {
         case KNNG_E_INTERNAL: return "KNNG_E_INTERNAL";
     }
     return "unknown";
+}
+
+knng_status knng_set_option(const char* name, int64_t value) {
+    if (!name) return fail(KNNG_E_USAGE, "null option name");
+    if (strcmp(name, "exact_u8") == 0) {
+        g_opt_exact_u8.store(value ? 1 : 0);
+        return KNNG_OK;
+    }
+    if (strcmp(name, "join_kernel") == 0) {
+        if (value < 0 || value > 1) return fail(KNNG_E_USAGE, "join_kernel must be 0 or 1");
+        g_opt_join_kernel.store(static_cast<int>(value));
+        return KNNG_OK;
+    }
+    return fail(KNNG_E_USAGE, "unknown or read-only option '%s'", name);
+}
+
+knng_status knng_get_option(const char* name, int64_t* host_value) {
+    if (!name || !host_value) return fail(KNNG_E_USAGE, "null argument");
+    if (strcmp(name, "exact_u8") == 0) *host_value = g_opt_exact_u8.load();
+    else if (strcmp(name, "join_kernel") == 0) *host_value = g_opt_join_kernel.load();
+    else if (strcmp(name, "last_exact_u8") == 0) *host_value = g_last_exact_u8;
+    else return fail(KNNG_E_USAGE, "unknown option '%s'", name);
+    return KNNG_OK;
 }
 
 int32_t knng_abi_version(void) { return 1; }

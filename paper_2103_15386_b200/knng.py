@@ -55,6 +55,8 @@ SIGNATURES = [
     ("knng_debug_iterate", i32, [P, i32, i64, i32, i32, i32, i32, u32, u64, i64, P, P, P, P, sz, P]),
     ("knng_debug_sample", i32, [i64, i32, i32, u32, u64, P, P, P, P, P, P, P, sz, P]),
     ("knng_debug_philox", i32, [P, i64, u64, P, P]),
+    ("knng_set_option", i32, [C.c_char_p, i64]),
+    ("knng_get_option", i32, [C.c_char_p, P]),
     ("knng_last_stats", i32, [P, i32]),
     ("knng_launch_count", i64, []),
     ("knng_set_timing", None, [i32]),
@@ -258,6 +260,16 @@ def knng_kernel_time(name: str) -> tuple[float, int]:
     cnt = C.c_int64()
     lib().knng_kernel_time(name.encode(), C.addressof(ms), C.addressof(cnt))
     return ms.value, cnt.value
+
+
+def knng_set_option(name: str, value: int):
+    _check(lib().knng_set_option(name.encode(), int(value)))
+
+
+def knng_get_option(name: str) -> int:
+    v = C.c_int64()
+    _check(lib().knng_get_option(name.encode(), C.addressof(v)))
+    return v.value
 
 
 def knng_last_error() -> str:

@@ -176,3 +176,38 @@ def test_bruteforce_bit_exact(K, shape, n, d, dtype, metric):
     gi, gd = K.knng_bruteforce(dev(X), dev(q), 10, metric)
     assert np.array_equal(gi.cpu().numpy().view(np.uint32), orc.key_ids(o))
     assert np.array_equal(gd.cpu().numpy(), orc.key_dists(o))
+
+
+def test_exact_u8_path_is_bit_identical_to_the_float_path(K):
+    # option exact_u8 (include/knng.h): integer-valued float32 data in
+    # [0, 255] with d <= 258 runs on an exact uint8 copy; both paths must
+    # produce the oracle's graph bit for bit.
+    X = datagen.make("sift", 5000, seed=9)  # integer-valued fp32
+    oi, od = orc.build(X, 32, 16, 6, 5)
+    Xd = dev(X)
+    try:
+        for opt in (1, 0):
+            K.knng_set_option("exact_u8", opt)
+            gi, gd = K.knng_build(Xd, 32, 6, 16, 5)
+            assert K.knng_get_option("last_exact_u8") == opt
+            assert np.array_equal(gi.cpu().numpy().view(np.uint32), oi)
+            assert np.array_equal(gd.cpu().numpy(), od)
+        # non-integer data never takes the integer path
+        K.knng_set_option("exact_u8", 1)
+        Y = X + np.float32(0.5)
+        K.knng_build(dev(Y), 32, 2, 16, 5)
+        assert K.knng_get_option("last_exact_u8") == 0
+    finally:
+        K.knng_set_option("exact_u8", 1)
+
+
+def test_legacy_join_kernel_matches(K):
+    X = datagen.make("c1", 3000, seed=4)
+    oi, od = orc.build(X, 10, 8, 6, 2)
+    try:
+        K.knng_set_option("join_kernel", 1)
+        gi, gd = K.knng_build(dev(X), 10, 6, 8, 2)
+        assert np.array_equal(gi.cpu().numpy().view(np.uint32), oi)
+        assert np.array_equal(gd.cpu().numpy(), od)
+    finally:
+        K.knng_set_option("join_kernel", 0)
