@@ -205,6 +205,21 @@ template <>
 struct Canon<uint8_t> {
     __device__ static __forceinline__ float l2(const uint8_t* __restrict__ a,
                                                const uint8_t* __restrict__ b, int d) {
+        if ((d & 15) == 0 && ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0) {
+            // integer sums are exact in any order: 16 dims per 128-bit load
+            unsigned int acc = 0;
+            const uint4* a4 = reinterpret_cast<const uint4*>(a);
+            const uint4* b4 = reinterpret_cast<const uint4*>(b);
+            for (int i = 0; i < (d >> 4); ++i) {
+                const uint4 x = __ldg(a4 + i), y = __ldg(b4 + i);
+                uint32_t t;
+                t = __vabsdiffu4(x.x, y.x); acc = __dp4a(t, t, acc);
+                t = __vabsdiffu4(x.y, y.y); acc = __dp4a(t, t, acc);
+                t = __vabsdiffu4(x.z, y.z); acc = __dp4a(t, t, acc);
+                t = __vabsdiffu4(x.w, y.w); acc = __dp4a(t, t, acc);
+            }
+            return static_cast<float>(acc);
+        }
         int acc = 0;
         for (int i = 0; i < d; ++i) {
             const int t = static_cast<int>(__ldg(a + i)) - static_cast<int>(__ldg(b + i));

@@ -22,8 +22,9 @@
 //      minima (packed (d, id) keys, D3) in a double-buffered partials area.
 //  epilogue (3 warps): GetNearestObject (Alg. 2) per output slot -- the min
 //      over the partials of the blocks covering the sample (the paper's
-//      atomicMin on (v, d), without atomics) -- and the 2m+q keys of
-//      every node to S.cand; then releases the partials and metadata.
+//      atomicMin on (v, d), without atomics) -- and files the 2m+q
+//      keys of every node into their targets' buckets (the k_cand_scatter
+//      step, fused); then releases the partials and metadata.
 //
 // Consumers never wait for each other: the selection/output epilogue of
 // batch b runs on its own warps while batch b+1 is computed, and the
@@ -44,6 +45,8 @@ constexpr int kWsSlots = 256;    // sample rows per stage (all nodes of a batch)
 constexpr int kWsBlocks = kWsConsumerWarps * 32;  // 4x4 blocks per batch
 constexpr int kWsMaxNodes = 32;  // nodes per batch (one producer chunk)
 constexpr int kWsMeta = 3;
+// selected keys per batch <= sum(2m + q) <= 2 * slots: rounds of the epilogue
+constexpr int kEpiRounds = (2 * kWsSlots + kWsEpiThreads - 1) / kWsEpiThreads;
 
 struct WsMeta {
     int nnodes;   // 0 = no more work
@@ -52,6 +55,7 @@ struct WsMeta {
     int pad_;
     int64_t x[kWsMaxNodes];
     int m[kWsMaxNodes], q[kWsMaxNodes], sbase[kWsMaxNodes], bbase[kWsMaxNodes + 1];
+    int obase[kWsMaxNodes + 1];  // prefix of the 2m+q selected keys per node
     uint32_t ids[kWsSlots];
 };
 
@@ -111,7 +115,8 @@ struct WsCfg {
     static constexpr size_t kMetaOff = kStageBytes * STAGES;
     static constexpr size_t kPartOff = (kMetaOff + sizeof(WsMeta) * kWsMeta + 15) & ~size_t(15);
     static constexpr size_t kPartBytes = sizeof(unsigned long long) * 8 * kWsBlocks;  // row + col minima
-    static constexpr size_t kBarOff = kPartOff + 2 * kPartBytes;
+    static constexpr size_t kEpiOff = kPartOff + 2 * kPartBytes;  // epilogue key/target staging
+    static constexpr size_t kBarOff = kEpiOff + (8 + 4) * kEpiRounds * kWsEpiThreads;
     static constexpr int kNumBars = 2 * STAGES + 2 * kWsMeta + 4;
     static constexpr size_t kSmem = kBarOff + 8 * kNumBars;
 };
@@ -123,7 +128,7 @@ __device__ int g_join_dbg = 0;
 
 template <typename T, bool COS, int STAGES>
 __global__ void __launch_bounds__(kWsThreads, 1)
-k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Samples S, int64_t boundary,
+k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G, Samples S, int64_t boundary,
           unsigned long long* __restrict__ work, DevStats* __restrict__ stats) {
     using Cfg = WsCfg<T, COS, STAGES>;
     using E = typename Cfg::E;
@@ -136,6 +141,8 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Samples
     E* ring = reinterpret_cast<E*>(ws_smem);
     WsMeta* meta = reinterpret_cast<WsMeta*>(ws_smem + Cfg::kMetaOff);
     unsigned long long* parts = reinterpret_cast<unsigned long long*>(ws_smem + Cfg::kPartOff);  // [2][8][blocks]
+    unsigned long long* ep_key = reinterpret_cast<unsigned long long*>(ws_smem + Cfg::kEpiOff);
+    uint32_t* ep_tgt = reinterpret_cast<uint32_t*>(ep_key + kEpiRounds * kWsEpiThreads);
     uint64_t* bars = reinterpret_cast<uint64_t*>(ws_smem + Cfg::kBarOff);
     uint64_t* full = bars;                          // [STAGES]  producers -> consumers
     uint64_t* empty = bars + STAGES;                // [STAGES]  consumers -> producers
@@ -174,6 +181,7 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Samples
     if (warp < kWsEpilogueWarps) {
         // ================================ epilogue ===============================
         const int et = tid;
+        unsigned long long n_cand = 0, n_app = 0;
         for (uint32_t b = 0;; ++b) {
             const int mb = b % kWsMeta, pb = b & 1;
             mbar_wait_sleep(mfull + mb, (b / kWsMeta) & 1);
@@ -183,14 +191,20 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Samples
             mbar_wait_sleep(pfull + pb, (b >> 1) & 1);
             const unsigned long long* rowp = parts + pb * 8 * kWsBlocks;
             const unsigned long long* colp = rowp + 4 * kWsBlocks;
-            // slot j of node x: c_nn(u_j) (j < m), c_no(u_j) (j < 2m), c_on(w_j)
-            for (int idx = et; idx < nn * 96; idx += kWsEpiThreads) {
-                const int i = idx / 96, j = idx - i * 96;
+            // output o of the batch is key j of node i (obase[i] <= o): c_nn(u_j)
+            // (j < m), c_no(u_{j-m}) (j < 2m), c_on(w_{j-2m})
+            const int total = M.obase[nn];
+            for (int r = 0; r < kEpiRounds; ++r) {
+                const int o = et + r * kWsEpiThreads;
+                uint64_t v = kSentinel;
+                uint32_t tgt = 0;
+                if (o < total) {
+                int i = 0;
+                while (i + 1 < nn && M.obase[i + 1] <= o) ++i;
+                const int j = o - M.obase[i];
                 const int mi = M.m[i], qi = M.q[i];
-                if (j >= 2 * mi + qi) continue;
                 const int mgi = (mi + 3) >> 2, qgi = (qi + 3) >> 2, bb = M.bbase[i];
                 const int nnn_i = mgi * (mgi + 1) / 2;
-                uint64_t v = kSentinel;
                 if (j < 2 * mi) {
                     const int u = j < mi ? j : j - mi, I = u >> 2, r = u & 3;
                     if (j < mi) {  // as a row of blocks (I, J <= I) and a column of (I' >= I, I)
@@ -215,13 +229,54 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Samples
                         v = t < v ? t : v;
                     }
                 }
-                S.cand[static_cast<size_t>(M.x[i]) * (3 * cap) + j] = v;
+                // target: the NEW sample u_j (c_nn, c_no) or OLD sample w_j (c_on)
+                const int sbi = M.sbase[i], mpi = (mi + 3) & ~3;
+                tgt = M.ids[j < mi ? sbi + j : (j < 2 * mi ? sbi + j - mi : sbi + mpi + j - 2 * mi)];
+                }
+                ep_key[r * kWsEpiThreads + et] = v;
+                ep_tgt[r * kWsEpiThreads + et] = tgt;
             }
+            // file the keys into their targets' buckets (the k_cand_scatter
+            // step, fused); keys >= the target's iteration-start k-th key
+            // cannot enter (exact, D17).  All loads, then all atomics, then
+            // all stores: kEpiRounds independent chains per thread in flight.
+            uint64_t kv[kEpiRounds], th[kEpiRounds], bo[kEpiRounds];
+            uint32_t tg[kEpiRounds], sl[kEpiRounds];
+#pragma unroll
+            for (int r = 0; r < kEpiRounds; ++r) {
+                kv[r] = ep_key[r * kWsEpiThreads + et];
+                tg[r] = ep_tgt[r * kWsEpiThreads + et];
+                th[r] = 0;
+                bo[r] = 0;
+                if (kv[r] != kSentinel) {  // D15: (inf, inf) inserts nothing
+                    th[r] = __ldg(G.kth + tg[r]);
+                    bo[r] = __ldg(G.boff + tg[r]);
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < kEpiRounds; ++r) {
+                n_cand += kv[r] != kSentinel;
+                const bool ok = kv[r] != kSentinel && kv[r] < th[r];
+                n_app += ok;
+                sl[r] = ok ? atomicAdd(G.bcnt + tg[r], 1u) : 0xFFFFFFFFu;
+            }
+#pragma unroll
+            for (int r = 0; r < kEpiRounds; ++r)
+                if (sl[r] != 0xFFFFFFFFu) G.bucket[bo[r] + sl[r]] = kv[r];
             named_bar(2, kWsEpiThreads);
             if (et == 0) {
                 mbar_arrive(pempty + pb);
                 mbar_arrive(mempty + mb);
             }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            n_cand += __shfl_xor_sync(kFull, n_cand, o);
+            n_app += __shfl_xor_sync(kFull, n_app, o);
+        }
+        if (lane == 0) {
+            if (n_cand) atomicAdd(&stats->candidates, n_cand);
+            if (n_app) atomicAdd(&stats->appended, n_app);
         }
         return;
     }
@@ -327,13 +382,22 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Samples
             WsMeta& M = meta[mb];
             const int nn = end - first;
             const int excl_b = cb - (pending ? my_nb : 0), excl_s = cs - (pending ? my_sl : 0);
-            if (static_cast<int>(lane) >= first && static_cast<int>(lane) < end) {
+            const bool in_batch = static_cast<int>(lane) >= first && static_cast<int>(lane) < end;
+            int co = in_batch ? 2 * my_m + my_q : 0;  // selected keys per node
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int tc = __shfl_up_sync(kFull, co, o);
+                if (static_cast<int>(lane) >= o) co += tc;
+            }
+            const int no_tot = __shfl_sync(kFull, co, end - 1);
+            if (in_batch) {
                 const int i = lane - first;
                 M.x[i] = x0 + lane;
                 M.m[i] = my_m;
                 M.q[i] = my_q;
                 M.sbase[i] = excl_s;
                 M.bbase[i] = excl_b;
+                M.obase[i] = co - (2 * my_m + my_q);
                 if (my_m > 0) {
                     ++n_joins;
                     n_m += my_m;
@@ -345,6 +409,7 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Samples
                 M.nblocks = nb_tot;
                 M.nslots = ns_tot;
                 M.bbase[nn] = nb_tot;
+                M.obase[nn] = no_tot;
             }
             __syncwarp();  // node table visible to the whole warp
             // sample ids of every slot of the batch, all loads independent

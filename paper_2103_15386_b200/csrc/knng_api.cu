@@ -321,7 +321,8 @@ struct Run {
         });
     }
 
-    void join(int iter) {
+    // returns true when the candidates were filed inside the join kernel
+    bool join(int iter) {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
         const int64_t batches = (D.n + kJoinNodes - 1) / kJoinNodes;
@@ -349,20 +350,20 @@ struct Run {
                 if (metric == KNNG_COSINE) {
                     constexpr size_t sm = WsCfg<float, true, STG>::kSmem;
                     cudaFuncSetAttribute(k_join_ws<float, true, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-                    k_join_ws<float, true, STG><<<sms, kWsThreads, sm, c.stream>>>(nullptr, Xn, D, S, boundary, work, st);
+                    k_join_ws<float, true, STG><<<sms, kWsThreads, sm, c.stream>>>(nullptr, Xn, D, G, S, boundary, work, st);
                 } else if (dt == KNNG_F32) {
                     constexpr size_t sm = WsCfg<float, false, STG>::kSmem;
                     cudaFuncSetAttribute(k_join_ws<float, false, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
                     k_join_ws<float, false, STG><<<sms, kWsThreads, sm, c.stream>>>(static_cast<const float*>(X), nullptr, D,
-                                                                                    S, boundary, work, st);
+                                                                                    G, S, boundary, work, st);
                 } else {
                     constexpr size_t sm = WsCfg<uint8_t, false, STG>::kSmem;
                     cudaFuncSetAttribute(k_join_ws<uint8_t, false, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
                     k_join_ws<uint8_t, false, STG><<<sms, kWsThreads, sm, c.stream>>>(static_cast<const uint8_t*>(X), nullptr,
-                                                                                      D, S, boundary, work, st);
+                                                                                      D, G, S, boundary, work, st);
                 }
             });
-            return;
+            return true;
         }
         c.launch("k_join", [&] {
             if (metric == KNNG_COSINE) {
@@ -381,6 +382,7 @@ struct Run {
                                                                            S, boundary, al, st);
             }
         });
+        return false;
     }
 
     void scatter(int iter) {
@@ -394,8 +396,7 @@ struct Run {
     void iteration(int iter, uint32_t tword, bool merge_first) {
         merge_sample(merge_first ? 1 : 0, 1, merge_first ? iter - 1 : -1);
         reverse(tword);
-        join(iter);
-        scatter(iter);
+        if (!join(iter)) scatter(iter);
     }
 
     void export_graph(uint32_t* ids, float* dists) {
