@@ -61,7 +61,8 @@ __device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
     return __shfl_xor_sync(kFull, v, m);
 }
 
-// Bitonic sort of one u64 per lane, ascending across lanes 0..31.
+// Bitonic sort of one u64 per lane, ascending across lanes 0..31.  Each
+// compare-exchange is one comparison and one select (branch-free).
 __device__ __forceinline__ uint64_t warp_sort_u64(uint64_t x) {
     const uint32_t lane = lane_id();
 #pragma unroll
@@ -69,13 +70,79 @@ __device__ __forceinline__ uint64_t warp_sort_u64(uint64_t x) {
 #pragma unroll
         for (int j = k2 >> 1; j > 0; j >>= 1) {
             const uint64_t o = shfl_xor_u64(x, j);
-            const bool up = (lane & k2) == 0;
-            const bool lower = (lane & j) == 0;
-            const uint64_t mn = o < x ? o : x, mx = o < x ? x : o;
-            x = (lower == up) ? mn : mx;
+            const bool keep_min = ((lane & j) == 0) == ((lane & k2) == 0);
+            x = (keep_min ? (o < x) : (x < o)) ? o : x;
         }
     }
     return x;
+}
+__device__ __forceinline__ uint32_t warp_sort_u32(uint32_t x) {
+    const uint32_t lane = lane_id();
+#pragma unroll
+    for (int k2 = 2; k2 <= 32; k2 <<= 1) {
+#pragma unroll
+        for (int j = k2 >> 1; j > 0; j >>= 1) {
+            const uint32_t o = __shfl_xor_sync(kFull, x, j);
+            const bool keep_min = ((lane & j) == 0) == ((lane & k2) == 0);
+            x = keep_min ? min(o, x) : max(o, x);
+        }
+    }
+    return x;
+}
+// bitonic sequence across the warp -> ascending
+__device__ __forceinline__ uint64_t warp_bitonic_merge_u64(uint64_t x) {
+    const uint32_t lane = lane_id();
+#pragma unroll
+    for (int j = 16; j > 0; j >>= 1) {
+        const uint64_t o = shfl_xor_u64(x, j);
+        x = (((lane & j) == 0) ? (o < x) : (x < o)) ? o : x;
+    }
+    return x;
+}
+
+// k-NN list update on one warp (D16-D17), branch-free: the list is
+// one (key, bits) per lane, ascending, unique, kSentinel-padded; bits =
+// bit0 NEW flag | bit1 entered from a bucket.  cand: up to 32 candidate keys
+// (any order, repeats allowed, kSentinel = none).  Result: the 32 smallest
+// unique keys of the union, ascending; list entries keep their bits,
+// newcomers get NEW | from-bucket.  Keys are compared as (key << 1) | origin
+// (origin 0 = list, 1 = candidate): dist >= 0 leaves bit 63 free, so the
+// shifted order is (dist, id, origin), and duplicates keep the list entry.
+__device__ __forceinline__ void warp_merge_list(uint64_t& L, uint32_t& bits, uint64_t cand) {
+    const uint32_t lane = lane_id();
+    uint64_t x = cand == kSentinel ? kSentinel : ((cand << 1) | 1ull);
+    x = warp_sort_u64(x);
+    const uint64_t l = L == kSentinel ? kSentinel : (L << 1);
+    const uint64_t xr = shfl_u64(x, 31 - lane);  // half-cleaner of l ++ reverse(x)
+    uint64_t lo = xr < l ? xr : l;
+    uint64_t hi = xr < l ? l : xr;
+    lo = warp_bitonic_merge_u64(lo);
+    hi = warp_bitonic_merge_u64(hi);
+    // dedup: adjacent equal keys (ignoring the origin bit) over lo ++ hi
+    const uint64_t lo_prev = shfl_u64(lo, (lane + 31) & 31);
+    const uint64_t lo_last = shfl_u64(lo, 31);  // every lane shuffles (no divergent shfl)
+    const uint64_t hi_prev_raw = shfl_u64(hi, (lane + 31) & 31);
+    const uint64_t hi_prev = lane == 0 ? lo_last : hi_prev_raw;
+    const bool lo_ok = lo != kSentinel && (lane == 0 || (lo >> 1) != (lo_prev >> 1));
+    const bool hi_ok = hi != kSentinel && (hi >> 1) != (hi_prev >> 1);
+    const uint32_t lo_m = __ballot_sync(kFull, lo_ok), hi_m = __ballot_sync(kFull, hi_ok);
+    const int nlo = __popc(lo_m);
+    // compaction: output lane j takes the j-th surviving element
+    const int j = static_cast<int>(lane);
+    const int src_lo = j < nlo ? static_cast<int>(__fns(lo_m, 0, j + 1)) : 0;
+    const int jh = j - nlo;
+    const int src_hi = (jh >= 0 && jh < __popc(hi_m)) ? static_cast<int>(__fns(hi_m, 0, jh + 1)) : 0;
+    const uint64_t from_lo = shfl_u64(lo, src_lo), from_hi = shfl_u64(hi, src_hi);
+    uint64_t e = kSentinel;
+    if (j < nlo) e = from_lo;
+    else if (jh < __popc(hi_m)) e = from_hi;
+    // bits: a list-origin element is the r-th list element kept, r = number
+    // of list-origin elements before it (the merge preserves their order)
+    const bool is_list = e != kSentinel && !(e & 1ull);
+    const int r = __popc(__ballot_sync(kFull, is_list) & lanemask_lt());
+    const uint32_t old_bits = __shfl_sync(kFull, bits, r);
+    bits = is_list ? old_bits : (e != kSentinel ? 3u : 0u);
+    L = e == kSentinel ? kSentinel : (e >> 1);
 }
 
 // Element of the list-merge network: key + meta (bit0 = NEW flag, bit1 =

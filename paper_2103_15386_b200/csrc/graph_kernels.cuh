@@ -104,10 +104,8 @@ __global__ void k_init(const T* __restrict__ X, const float* __restrict__ Xn, Di
 //             for the CSR of P:149.
 __global__ void k_merge_sample(Dims D, Graph G, Samples S, int do_merge, int do_sample,
                                DevStats* __restrict__ prev_stats) {
-    extern __shared__ Elem smem_scratch[];
     const int64_t s = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (s >= D.n) return;
-    Elem* scratch = smem_scratch + (threadIdx.x >> 5) * 32;
     const uint32_t lane = lane_id();
     const int k = D.k, p = D.p;
     const bool in_list = static_cast<int>(lane) < k;
@@ -121,7 +119,7 @@ __global__ void k_merge_sample(Dims D, Graph G, Samples S, int do_merge, int do_
             const uint64_t* bk = G.bucket + G.boff[s];
             for (uint32_t base = 0; base < c; base += 32) {
                 const uint64_t cand = (base + lane < c) ? bk[base + lane] : kSentinel;
-                warp_merge_chunk(cur, cand, scratch);
+                warp_merge_list(cur.key, cur.meta, cand);
             }
             changed = true;
             if (!in_list) cur = Elem{kSentinel, 0u};
@@ -251,30 +249,18 @@ __global__ void k_rev_scatter(Dims D, Samples S) {
     S.rsrc[static_cast<size_t>(f) * D.n * D.p + S.off[f * (D.n + 1) + v] + pos] = static_cast<uint32_t>(s);
 }
 
-__device__ __forceinline__ uint64_t warp_bitonic_merge_u64(uint64_t x) {
-    const uint32_t lane = lane_id();
-#pragma unroll
-    for (int j = 16; j > 0; j >>= 1) {
-        const uint64_t o = shfl_xor_u64(x, j);
-        const bool lower = (lane & j) == 0;
-        x = lower ? (o < x ? o : x) : (o < x ? x : o);
-    }
-    return x;
-}
-
-// sort + dedup one u32 id per lane (0xFFFFFFFF = empty); returns the unique
-// sorted ids compacted to lanes [0, count) and sets count.
+// sort + dedup one u32 id per lane (0xFFFFFFFF = empty, sorts last); returns
+// the unique sorted ids compacted to lanes [0, count) and sets count.
 __device__ __forceinline__ uint32_t warp_sort_unique_ids(uint32_t id, int& count) {
     const uint32_t lane = lane_id();
-    uint64_t x = id == 0xFFFFFFFFu ? kSentinel : static_cast<uint64_t>(id);
-    x = warp_sort_u64(x);
-    const uint64_t prev = shfl_u64(x, (lane + 31) & 31);
-    const bool ok = x != kSentinel && (lane == 0 || x != prev);
+    const uint32_t x = warp_sort_u32(id);
+    const uint32_t prev = __shfl_sync(kFull, x, (lane + 31) & 31);
+    const bool ok = x != 0xFFFFFFFFu && (lane == 0 || x != prev);
     const uint32_t okm = __ballot_sync(kFull, ok);
     count = __popc(okm);
     const int src = static_cast<int>(lane) < count ? static_cast<int>(__fns(okm, 0, lane + 1)) : 0;
-    const uint64_t got = shfl_u64(x, src);
-    return static_cast<int>(lane) < count ? static_cast<uint32_t>(got) : 0xFFFFFFFFu;
+    const uint32_t got = __shfl_sync(kFull, x, src);
+    return static_cast<int>(lane) < count ? got : 0xFFFFFFFFu;
 }
 
 // One warp per node v: G(v) = sort_unique(F(v) U c smallest-priority reverse
