@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--n", type=int, default=1_000_000)
     ap.add_argument("--k", type=int, default=32)
     ap.add_argument("--p", type=int, default=16)
-    ap.add_argument("--iters", type=int, default=8)
+    ap.add_argument("--iters", type=int, default=7)
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--recall-nodes", type=int, default=10_000)
     ap.add_argument("--cpu-sample", type=int, default=20_000)
@@ -264,21 +264,43 @@ def main():
         e2e = {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(X.nbytes),
                "d2h_bytes_per_step": int(n * args.k * 8)}
 
-    # ---- roofline of the dominant kernel (k_join): algorithmic bytes
+    # ---- roofline of the dominant kernel (k_join), DESIGN.md section 6:
+    # HBM view: algorithmic gather bytes = rows x (d x element + 4 id bytes);
+    # ALU view: the canonical tile's minimum instruction count -- f32: FADD +
+    # FFMA per dim and pair; exact-u8: VABSDIFF4 + IDP4A per 4 dims and pair
+    # -- against the SM issue peak (148 SMs x 4 warp-instr/cycle x clock).
+    exact_u8 = bool(K.knng_get_option("last_exact_u8"))
+    esz = 1 if exact_u8 else 4
+    nst = max(1, len(stats))
     rows = sum(s["rows"] for s in stats)
     evals = sum(s["dist_evals"] for s in stats)
-    alg_bytes_per_launch = rows * (d * 4 + 4) / max(1, len(stats))
+    alg_bytes_per_launch = rows * (d * esz + 4) / nst
     join_avg_ms = join_ms / max(1, join_launches)
     achieved_gbs = alg_bytes_per_launch / (join_avg_ms * 1e-3) / 1e9 if join_avg_ms > 0 else 0.0
     peak, peak_kind = peaks()
-    alu_tflops = evals * d * 3 / max(1, len(stats)) / (join_avg_ms * 1e-3) / 1e12 if join_avg_ms > 0 else 0.0
+    instr_per_dim_pair = 0.5 if exact_u8 else 2.0
+    warp_instr = evals * d * instr_per_dim_pair / 32 / nst
+    clk_ghz = (clk.get("sm_mhz") or 1965.0) / 1000.0
+    issue_peak = 148 * 4 * clk_ghz * 1e9
+    issue_rate = warp_instr / (join_avg_ms * 1e-3) if join_avg_ms > 0 else 0.0
+    traffic = None
+    try:  # dram__bytes_read.sum + dram__bytes_write.sum of one ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "join_traffic.json")) as f:
+            tj = json.load(f)
+        traffic = tj.get("u8" if exact_u8 else "f32")
+    except Exception:
+        pass
+    hbm_frac = achieved_gbs / peak
+    alu_frac = issue_rate / issue_peak
+    alu = {"bound": "alu", "achieved": issue_rate / 1e9, "peak": issue_peak / 1e9,
+           "unit": "G warp-instr/s", "frac": alu_frac,
+           "instr_per_dim_pair": instr_per_dim_pair, "sm_clock_ghz": clk_ghz}
     roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
-                "frac": achieved_gbs / peak, "traffic": None, "peak_source": peak_kind,
+                "frac": hbm_frac, "traffic": traffic, "peak_source": peak_kind,
                 "kernel": "k_join", "avg_launch_ms": join_avg_ms, "launches": join_launches,
                 "share_of_step": join_ms / args.steps / ms if ms > 0 else None,
-                "alg_bytes_per_launch": alg_bytes_per_launch,
-                "alu": {"achieved_tflops": alu_tflops, "peak_tflops": FP32_PEAK_TFLOPS,
-                        "frac": alu_tflops / FP32_PEAK_TFLOPS, "flops_per_dim_pair": 3}}
+                "alg_bytes_per_launch": alg_bytes_per_launch, "element_bytes": esz,
+                "alu": alu}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -288,8 +310,10 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": ms / 1000.0, "unit": "s", "n_gpus": world, "steps": args.steps,
                 "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f32",
-                "data": "synthetic GMM-LR SIFT-shaped (datagen 'sift', seed 1+rank), integer-valued fp32",
+                "vs_baseline": None, "dtype": "u8" if exact_u8 else "f32",
+                "data": "synthetic GMM-LR SIFT-shaped (datagen 'sift', seed 1+rank), integer-valued fp32 input"
+                        + ("; built on the exact uint8 path (option exact_u8: graph bit-identical to fp32)"
+                           if exact_u8 else ""),
                 "config": {"workload": "C2 SIFT1M-shaped (BASELINE.json configs[1])", "n": n, "d": d,
                            "k": args.k, "sample_size": args.p, "iters": args.iters, "metric": "l2",
                            "l2_flush": "inputs (512 MB) larger than L2", "per_rank": "one 1M build per GPU"},

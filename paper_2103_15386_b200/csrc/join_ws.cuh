@@ -1,16 +1,16 @@
 // join_ws.cuh -- warp-specialised local join (Alg. 1 lines 9-31).
 //
 // Same computation as k_join (join_kernel.cuh), organised as a three-role
-// pipeline for sm_100a (one persistent CTA per SM, 16 warps; consumers on
-// the highest warp ids, which the issue arbiter serves first):
+// pipeline for sm_100a (one persistent CTA per SM, 16 warps; the light roles
+// on the highest warp ids, which the issue arbiter serves first):
 //
-//  producers (5 warps): the lead warp grabs chunks of 32 nodes from a global
+//  producers (4 warps): the lead warp grabs chunks of 32 nodes from a global
 //      work counter and packs consecutive nodes into a batch whose 4x4
 //      register blocks fit the 256 consumer threads (one block each) and
 //      whose sample rows fit one ring stage; it publishes the batch metadata
 //      (node table, sample ids) into a kWsMeta-deep ring, running ahead of
-//      the rest.  4 gather warps issue the 16-B cp.async copies of each 32-dim slab of the batch's rows
-//      into a STAGES-deep ring; each thread signals completion with
+//      the rest.  3 gather warps issue the 16-B cp.async copies of each
+//      128-B row slab of the batch's rows into a STAGES-deep ring; each thread signals completion with
 //      cp.async.mbarrier.arrive.noinc on the stage's full barrier.  (One
 //      cp.async.bulk per 128-B row slab was tried first: those copies
 //      serialise through uniform registers on the issuing warp, ~90 cycles
@@ -20,7 +20,7 @@
 //      (D5/D6) slab by slab as the ring fills, releases each stage with one
 //      arrive per warp, and leaves the block's 4 row minima and 4 column
 //      minima (packed (d, id) keys, D3) in a double-buffered partials area.
-//  epilogue (3 warps): GetNearestObject (Alg. 2) per output slot -- the min
+//  epilogue (2 groups of 2 warps, alternate batches): GetNearestObject (Alg. 2) per output slot -- the min
 //      over the partials of the blocks covering the sample (the paper's
 //      atomicMin on (v, d), without atomics) -- and files the 2m+q
 //      keys of every node into their targets' buckets (the k_cand_scatter
@@ -35,18 +35,21 @@
 namespace knng {
 
 constexpr int kWsConsumerWarps = 8;
-constexpr int kWsProducerWarps = 5;  // 1 lead (batch metadata) + 4 gather warps
+constexpr int kWsProducerWarps = 4;  // 1 lead (batch metadata) + 3 gather warps
 constexpr int kWsGatherWarps = kWsProducerWarps - 1;
-constexpr int kWsEpilogueWarps = 3;
+constexpr int kWsEpiGroups = 2;      // epilogue groups, alternating batches
+constexpr int kWsEpiGroupWarps = 2;
+constexpr int kWsEpilogueWarps = kWsEpiGroups * kWsEpiGroupWarps;
 constexpr int kWsProdThreads = kWsGatherWarps * 32;
-constexpr int kWsEpiThreads = kWsEpilogueWarps * 32;
+constexpr int kWsEpiThreads = kWsEpiGroupWarps * 32;  // threads of one epilogue group
 constexpr int kWsThreads = (kWsConsumerWarps + kWsProducerWarps + kWsEpilogueWarps) * 32;
 constexpr int kWsSlots = 256;    // sample rows per stage (all nodes of a batch)
 constexpr int kWsBlocks = kWsConsumerWarps * 32;  // 4x4 blocks per batch
 constexpr int kWsMaxNodes = 32;  // nodes per batch (one producer chunk)
-constexpr int kWsMeta = 3;
+constexpr int kWsMeta = 4;
 // selected keys per batch <= sum(2m + q) <= 2 * slots: rounds of the epilogue
 constexpr int kEpiRounds = (2 * kWsSlots + kWsEpiThreads - 1) / kWsEpiThreads;
+static_assert(kWsEpiGroups == 2, "partials are double-buffered: one buffer per epilogue group");
 
 struct WsMeta {
     int nnodes;   // 0 = no more work
@@ -116,7 +119,7 @@ struct WsCfg {
     static constexpr size_t kPartOff = (kMetaOff + sizeof(WsMeta) * kWsMeta + 15) & ~size_t(15);
     static constexpr size_t kPartBytes = sizeof(unsigned long long) * 8 * kWsBlocks;  // row + col minima
     static constexpr size_t kEpiOff = kPartOff + 2 * kPartBytes;  // epilogue key/target staging
-    static constexpr size_t kBarOff = kEpiOff + (8 + 4) * kEpiRounds * kWsEpiThreads;
+    static constexpr size_t kBarOff = kEpiOff + (8 + 4) * kEpiRounds * kWsEpiThreads * kWsEpiGroups;
     static constexpr int kNumBars = 2 * STAGES + 2 * kWsMeta + 4;
     static constexpr size_t kSmem = kBarOff + 8 * kNumBars;
 };
@@ -142,7 +145,7 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
     WsMeta* meta = reinterpret_cast<WsMeta*>(ws_smem + Cfg::kMetaOff);
     unsigned long long* parts = reinterpret_cast<unsigned long long*>(ws_smem + Cfg::kPartOff);  // [2][8][blocks]
     unsigned long long* ep_key = reinterpret_cast<unsigned long long*>(ws_smem + Cfg::kEpiOff);
-    uint32_t* ep_tgt = reinterpret_cast<uint32_t*>(ep_key + kEpiRounds * kWsEpiThreads);
+    uint32_t* ep_tgt = reinterpret_cast<uint32_t*>(ep_key + kEpiRounds * kWsEpiThreads * kWsEpiGroups);
     uint64_t* bars = reinterpret_cast<uint64_t*>(ws_smem + Cfg::kBarOff);
     uint64_t* full = bars;                          // [STAGES]  producers -> consumers
     uint64_t* empty = bars + STAGES;                // [STAGES]  consumers -> producers
@@ -176,13 +179,20 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
     }
     __syncthreads();
 
-    // warp roles: [0, E) epilogue, E lead producer, (E, E+P) gather warps,
-    // [E+P, 16) consumers (highest ids: first pick of the warp arbiter)
-    if (warp < kWsEpilogueWarps) {
+    // warp roles: [0, 8) consumers, [8, 11) gather, 11 lead, [12, 16) epilogue.
+    // The issue arbiter serves the highest warp id first: the light roles
+    // (which sleep when idle) get priority so they never starve the
+    // pipeline; the consumers take every remaining slot.
+    if (warp >= kWsConsumerWarps + kWsProducerWarps) {
         // ================================ epilogue ===============================
-        const int et = tid;
+        // kWsEpiGroups groups take alternate batches, so the filing latency
+        // of one batch overlaps the next one's
+        const int g = (warp - kWsConsumerWarps - kWsProducerWarps) / kWsEpiGroupWarps;
+        const int et = tid - (kWsConsumerWarps + kWsProducerWarps) * 32 - g * kWsEpiThreads;
+        unsigned long long* gkey = ep_key + g * kEpiRounds * kWsEpiThreads;
+        uint32_t* gtgt = ep_tgt + g * kEpiRounds * kWsEpiThreads;
         unsigned long long n_cand = 0, n_app = 0;
-        for (uint32_t b = 0;; ++b) {
+        for (uint32_t b = g;; b += kWsEpiGroups) {
             const int mb = b % kWsMeta, pb = b & 1;
             mbar_wait_sleep(mfull + mb, (b / kWsMeta) & 1);
             const WsMeta& M = meta[mb];
@@ -199,53 +209,60 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
                 uint64_t v = kSentinel;
                 uint32_t tgt = 0;
                 if (o < total) {
-                int i = 0;
-                while (i + 1 < nn && M.obase[i + 1] <= o) ++i;
-                const int j = o - M.obase[i];
-                const int mi = M.m[i], qi = M.q[i];
-                const int mgi = (mi + 3) >> 2, qgi = (qi + 3) >> 2, bb = M.bbase[i];
-                const int nnn_i = mgi * (mgi + 1) / 2;
-                if (j < 2 * mi) {
-                    const int u = j < mi ? j : j - mi, I = u >> 2, r = u & 3;
-                    if (j < mi) {  // as a row of blocks (I, J <= I) and a column of (I' >= I, I)
-                        for (int J = 0; J <= I; ++J) {
-                            const uint64_t t = rowp[(bb + I * (I + 1) / 2 + J) * 4 + r];
-                            v = t < v ? t : v;
+                    int i = 0;
+                    while (i + 1 < nn && M.obase[i + 1] <= o) ++i;
+                    const int j = o - M.obase[i];
+                    const int mi = M.m[i], qi = M.q[i];
+                    const int mgi = (mi + 3) >> 2, qgi = (qi + 3) >> 2, bb = M.bbase[i];
+                    const int nnn_i = mgi * (mgi + 1) / 2;
+                    if (j < 2 * mi) {
+                        const int u = j < mi ? j : j - mi, I = u >> 2, rr = u & 3;
+                        if (j < mi) {  // as a row of blocks (I, J <= I) and a column of (I' >= I, I)
+                            for (int J = 0; J <= I; ++J) {
+                                const uint64_t t = rowp[(bb + I * (I + 1) / 2 + J) * 4 + rr];
+                                v = t < v ? t : v;
+                            }
+                            for (int I2 = I; I2 < mgi; ++I2) {
+                                const uint64_t t = colp[(bb + I2 * (I2 + 1) / 2 + I) * 4 + rr];
+                                v = t < v ? t : v;
+                            }
+                        } else {  // rows of the NEW-OLD blocks (I, J)
+                            for (int J = 0; J < qgi; ++J) {
+                                const uint64_t t = rowp[(bb + nnn_i + I * qgi + J) * 4 + rr];
+                                v = t < v ? t : v;
+                            }
                         }
-                        for (int I2 = I; I2 < mgi; ++I2) {
-                            const uint64_t t = colp[(bb + I2 * (I2 + 1) / 2 + I) * 4 + r];
-                            v = t < v ? t : v;
-                        }
-                    } else {  // rows of the NEW-OLD blocks (I, J)
-                        for (int J = 0; J < qgi; ++J) {
-                            const uint64_t t = rowp[(bb + nnn_i + I * qgi + J) * 4 + r];
+                    } else {  // columns of the NEW-OLD blocks (I, J_w)
+                        const int oo = j - 2 * mi, J = oo >> 2, c = oo & 3;
+                        for (int I = 0; I < mgi; ++I) {
+                            const uint64_t t = colp[(bb + nnn_i + I * qgi + J) * 4 + c];
                             v = t < v ? t : v;
                         }
                     }
-                } else {  // columns of the NEW-OLD blocks (I, J_w)
-                    const int o = j - 2 * mi, J = o >> 2, c = o & 3;
-                    for (int I = 0; I < mgi; ++I) {
-                        const uint64_t t = colp[(bb + nnn_i + I * qgi + J) * 4 + c];
-                        v = t < v ? t : v;
-                    }
+                    // target: the NEW sample u_j (c_nn, c_no) or the OLD sample w_j (c_on)
+                    const int sbi = M.sbase[i], mpi = (mi + 3) & ~3;
+                    tgt = M.ids[j < mi ? sbi + j : (j < 2 * mi ? sbi + j - mi : sbi + mpi + j - 2 * mi)];
                 }
-                // target: the NEW sample u_j (c_nn, c_no) or OLD sample w_j (c_on)
-                const int sbi = M.sbase[i], mpi = (mi + 3) & ~3;
-                tgt = M.ids[j < mi ? sbi + j : (j < 2 * mi ? sbi + j - mi : sbi + mpi + j - 2 * mi)];
-                }
-                ep_key[r * kWsEpiThreads + et] = v;
-                ep_tgt[r * kWsEpiThreads + et] = tgt;
+                gkey[r * kWsEpiThreads + et] = v;
+                gtgt[r * kWsEpiThreads + et] = tgt;
+            }
+            // partials and metadata are no longer needed: release them so the
+            // consumers and the lead producer run ahead of the filing
+            named_bar(2 + g, kWsEpiThreads);
+            if (et == 0) {
+                mbar_arrive(pempty + pb);
+                mbar_arrive(mempty + mb);
             }
             // file the keys into their targets' buckets (the k_cand_scatter
             // step, fused); keys >= the target's iteration-start k-th key
             // cannot enter (exact, D17).  All loads, then all atomics, then
-            // all stores: kEpiRounds independent chains per thread in flight.
+            // all stores: kEpiRounds independent chains in flight per thread.
             uint64_t kv[kEpiRounds], th[kEpiRounds], bo[kEpiRounds];
             uint32_t tg[kEpiRounds], sl[kEpiRounds];
 #pragma unroll
             for (int r = 0; r < kEpiRounds; ++r) {
-                kv[r] = ep_key[r * kWsEpiThreads + et];
-                tg[r] = ep_tgt[r * kWsEpiThreads + et];
+                kv[r] = gkey[r * kWsEpiThreads + et];
+                tg[r] = gtgt[r * kWsEpiThreads + et];
                 th[r] = 0;
                 bo[r] = 0;
                 if (kv[r] != kSentinel) {  // D15: (inf, inf) inserts nothing
@@ -263,11 +280,6 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
 #pragma unroll
             for (int r = 0; r < kEpiRounds; ++r)
                 if (sl[r] != 0xFFFFFFFFu) G.bucket[bo[r] + sl[r]] = kv[r];
-            named_bar(2, kWsEpiThreads);
-            if (et == 0) {
-                mbar_arrive(pempty + pb);
-                mbar_arrive(mempty + mb);
-            }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -281,9 +293,9 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
         return;
     }
 
-    if (warp < kWsEpilogueWarps + kWsProducerWarps) {
+    if (warp >= kWsConsumerWarps) {
         // =============================== producers ==============================
-        const int ptid = tid - (kWsEpilogueWarps + 1) * 32;  // gather thread index
+        const int ptid = tid - kWsConsumerWarps * 32;  // gather thread index
         constexpr int CE = SlabCfg<T>::kChunkElems, CPR = SD / CE;
         uint32_t slab_it = 0, meta_it = 0;
         // each gather thread owns one 16-B chunk column of the slab and walks
@@ -324,7 +336,7 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
                 ++slab_it;
             }
         };
-        if (warp > kWsEpilogueWarps) {  // gather warps follow the batch stream
+        if (warp < kWsConsumerWarps + kWsGatherWarps) {  // gather warps follow the batch stream
             while (true) {
                 const int mb = meta_it % kWsMeta;
                 mbar_wait_sleep(mfull + mb, (meta_it / kWsMeta) & 1);
@@ -428,12 +440,16 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
             mbar_arrive(mfull + mb);  // all 32 lanes: releases every lane's writes
             ++meta_it;
         }
-        // termination marker
-        const int mb = meta_it % kWsMeta;
-        mbar_wait_sleep(mempty + mb, ((meta_it / kWsMeta) & 1) ^ 1);
-        if (lane == 0) meta[mb].nnodes = 0;
-        __syncwarp();
-        mbar_arrive(mfull + mb);
+        // termination markers: one per epilogue group (each group waits on
+        // its own batch sequence); consumers and gatherers stop at the first
+        for (int e = 0; e < kWsEpiGroups; ++e) {
+            const int mb = meta_it % kWsMeta;
+            mbar_wait_sleep(mempty + mb, ((meta_it / kWsMeta) & 1) ^ 1);
+            if (lane == 0) meta[mb].nnodes = 0;
+            __syncwarp();
+            mbar_arrive(mfull + mb);
+            ++meta_it;
+        }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             n_joins += __shfl_xor_sync(kFull, n_joins, o);
@@ -450,12 +466,12 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
     }
 
     // ================================ consumers =================================
-    const int ct = tid - (kWsEpilogueWarps + kWsProducerWarps) * 32;  // 0 .. kWsBlocks-1
+    const int ct = tid;  // 0 .. kWsBlocks-1
     uint32_t slab_it = 0;
     unsigned long long my_pairs = 0;
     for (uint32_t b = 0;; ++b) {
         const int mb = b % kWsMeta, pb = b & 1;
-        mbar_wait(mfull + mb, (b / kWsMeta) & 1);
+        mbar_wait_sleep(mfull + mb, (b / kWsMeta) & 1);
         const WsMeta& M = meta[mb];
         const int nn = M.nnodes;
         if (nn == 0) break;
@@ -560,7 +576,7 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
 
         // ---- block minima: 4 row keys (c_nn / c_no candidates of the NEW
         // rows) and 4 column keys (c_nn / c_on candidates of the columns)
-        mbar_wait(pempty + pb, ((b >> 1) & 1) ^ 1);
+        mbar_wait_sleep(pempty + pb, ((b >> 1) & 1) ^ 1);
         unsigned long long* rowp = parts + pb * 8 * kWsBlocks;
         unsigned long long* colp = rowp + 4 * kWsBlocks;
         if (active) {

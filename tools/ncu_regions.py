@@ -21,7 +21,7 @@ if len(sys.argv) < 3:
         if any(k in s for k in ("TRYWAIT", "BAR.SYNC", "EXIT", "ARRIVE", "LDGSTS", "ATOMG", "STG")):
             print(i, s.strip()[:70], r[Ex], r[A])
     sys.exit(0)
-cols = ["stall_long_sb", "stall_wait", "stall_short_sb", "stall_barrier", "stall_branch_resolving", "stall_selected",
+cols = ["stall_long_sb", "stall_wait", "stall_short_sb", "stall_barrier", "stall_sleep", "stall_selected",
         "stall_not_selected", "stall_dispatch", "stall_math", "stall_no_inst", "stall_lg", "stall_mio"]
 ci = [h.index(c) for c in cols]
 T = sum(float(r[A] or 0) for r in data)
