@@ -46,7 +46,7 @@ constexpr int kWsThreads = (kWsConsumerWarps + kWsProducerWarps + kWsEpilogueWar
 constexpr int kWsSlots = 256;    // sample rows per stage (all nodes of a batch)
 constexpr int kWsBlocks = kWsConsumerWarps * 32;  // 4x4 blocks per batch
 constexpr int kWsMaxNodes = 32;  // nodes per batch (one producer chunk)
-constexpr int kWsMeta = 4;
+constexpr int kWsMeta = 3;
 // selected keys per batch <= sum(2m + q) <= 2 * slots: rounds of the epilogue
 constexpr int kEpiRounds = (2 * kWsSlots + kWsEpiThreads - 1) / kWsEpiThreads;
 static_assert(kWsEpiGroups == 2, "partials are double-buffered: one buffer per epilogue group");
@@ -121,7 +121,12 @@ struct WsCfg {
     static constexpr size_t kEpiOff = kPartOff + 2 * kPartBytes;  // epilogue key/target staging
     static constexpr size_t kBarOff = kEpiOff + (8 + 4) * kEpiRounds * kWsEpiThreads * kWsEpiGroups;
     static constexpr int kNumBars = 2 * STAGES + 2 * kWsMeta + 4;
-    static constexpr size_t kSmem = kBarOff + 8 * kNumBars;
+    // lead's double-buffered chunk cache: (m, q) bytes of 32 nodes, then
+    // their Gn and Go sample-id rows (cap <= 2 * p_max = 32 ids each)
+    static constexpr size_t kCacheOff = (kBarOff + 8 * kNumBars + 15) & ~size_t(15);
+    static constexpr size_t kCacheBytes = 2 * 64 + 2 * 32 * 2 * 32 * sizeof(uint32_t);
+    static constexpr size_t kSmem = kCacheOff + kCacheBytes;
+    static_assert(kSmem <= 232448, "227 KB dynamic shared memory per CTA");
 };
 
 // Diagnostic switch (KNNG_JOIN_DBG, never set in tests or the bench):
@@ -348,29 +353,74 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
             return;
         }
         // lead producer: forms batches and publishes their metadata, running
-        // up to kWsMeta batches ahead of the gathers and the tiles
-        int64_t x0 = 0;
+        // up to kWsMeta batches ahead of the gathers and the tiles.  Chunks
+        // of 32 nodes are claimed two ahead, and the next chunk's counts and
+        // sample-id rows are prefetched with cp.async into a double-buffered
+        // chunk cache while the current chunk's batches are published, so
+        // publication never waits on global memory.
+        uint8_t* cc_cnt = ws_smem + Cfg::kCacheOff;                                      // [2][64]
+        uint32_t* cc_ids = reinterpret_cast<uint32_t*>(ws_smem + Cfg::kCacheOff + 128);  // [2][32][2cap]
+        int cur_buf = 0;
+        int64_t cur_x0 = 0;
+        auto claim = [&]() -> unsigned long long {
+            unsigned long long c0 = 0;
+            if (lane == 0) c0 = atomicAdd(work, 32ull);
+            return c0;  // lane 0's value; broadcast at use
+        };
+        auto fetch = [&](int buf, int64_t xb) {
+            if (xb < D.n) {
+                const int nodes = static_cast<int>(D.n - xb < 32 ? D.n - xb : 32);
+                uint8_t* ccnt = cc_cnt + buf * 64;
+                uint32_t* cids = cc_ids + static_cast<size_t>(buf) * 32 * 2 * cap;
+                if (lane < 16) {  // (m, q) byte pairs, 4 bytes per lane, zero-filled past n
+                    const int lo = 4 * lane, bytes = max(0, min(4, 2 * nodes - lo));
+                    const uint32_t s = smem_u32(ccnt + lo);
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s),
+                                 "l"(S.gcnt + 2 * xb + lo), "r"(bytes)
+                                 : "memory");
+                }
+                for (int e = lane; e < nodes * 2 * cap; e += 32) {
+                    const int node = e / (2 * cap), w = e - node * 2 * cap;
+                    const uint32_t* src = w < cap ? S.G + static_cast<size_t>(xb + node) * cap + w
+                                                  : S.G + static_cast<size_t>(D.n) * cap +
+                                                        static_cast<size_t>(xb + node) * cap + (w - cap);
+                    const uint32_t s = smem_u32(cids + e);
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(src) : "memory");
+                }
+            }
+            cp_async_commit();
+        };
+        int64_t x0 = static_cast<int64_t>(__shfl_sync(kFull, claim(), 0));
+        int64_t xnext = static_cast<int64_t>(__shfl_sync(kFull, claim(), 0));
+        int buf = 0;
+        fetch(0, x0);
         int cur = 32;  // position inside the current 32-node chunk
         int my_m = 0, my_q = 0, my_nb = 0, my_sl = 0;
         unsigned long long n_joins = 0, n_m = 0, n_q = 0;
         while (true) {
             if (cur >= 32) {
-                unsigned long long c0 = 0;
-                if (lane == 0) c0 = atomicAdd(work, 32ull);
-                x0 = static_cast<int64_t>(__shfl_sync(kFull, c0, 0));
                 if (x0 >= D.n) break;
+                const unsigned long long claimed = claim();  // used one chunk later
+                fetch(buf ^ 1, xnext);
+                cp_async_wait<1>();  // this chunk's group has landed
+                __syncwarp();  // every lane's copies of this chunk visible to all
                 const int64_t x = x0 + lane;
                 my_m = 0;
                 my_q = 0;
                 if (x < D.n) {
-                    my_m = S.gcnt[2 * x];
-                    my_q = S.gcnt[2 * x + 1];
+                    my_m = cc_cnt[buf * 64 + 2 * lane];
+                    my_q = cc_cnt[buf * 64 + 2 * lane + 1];
                 }
                 if (my_m == 0) my_q = 0;  // no NEW sample: nothing to join
                 const int mg = (my_m + 3) >> 2, qg = (my_q + 3) >> 2;
                 my_nb = mg * (mg + 1) / 2 + mg * qg;
                 my_sl = 4 * (mg + qg);
                 cur = 0;
+                cur_buf = buf;
+                cur_x0 = x0;
+                x0 = xnext;
+                xnext = static_cast<int64_t>(__shfl_sync(kFull, claimed, 0));
+                buf ^= 1;
             }
             // take nodes cur.. while the batch's blocks and slots fit
             const bool pending = static_cast<int>(lane) >= cur;
@@ -404,7 +454,7 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
             const int no_tot = __shfl_sync(kFull, co, end - 1);
             if (in_batch) {
                 const int i = lane - first;
-                M.x[i] = x0 + lane;
+                M.x[i] = cur_x0 + lane;
                 M.m[i] = my_m;
                 M.q[i] = my_q;
                 M.sbase[i] = excl_s;
@@ -424,22 +474,23 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
                 M.obase[nn] = no_tot;
             }
             __syncwarp();  // node table visible to the whole warp
-            // sample ids of every slot of the batch, all loads independent
+            // sample ids of every slot of the batch, from the chunk cache
+            const uint32_t* cids = cc_ids + static_cast<size_t>(cur_buf) * 32 * 2 * cap;
             for (int j = lane; j < ns_tot; j += 32) {
                 int i = 0;
                 while (i + 1 < nn && M.sbase[i + 1] <= j) ++i;
                 const int m = M.m[i], q = M.q[i], mpad = (m + 3) & ~3, js = j - M.sbase[i];
-                const int64_t x = M.x[i];
+                const uint32_t* row = cids + (first + i) * 2 * cap;
                 uint32_t id = 0xFFFFFFFFu;
-                if (js < m) id = S.G[static_cast<size_t>(x) * cap + js];
-                else if (js >= mpad && js - mpad < q)
-                    id = S.G[static_cast<size_t>(D.n) * cap + static_cast<size_t>(x) * cap + (js - mpad)];
+                if (js < m) id = row[js];
+                else if (js >= mpad && js - mpad < q) id = row[cap + (js - mpad)];
                 M.ids[j] = id;
             }
             __syncwarp();
             mbar_arrive(mfull + mb);  // all 32 lanes: releases every lane's writes
             ++meta_it;
         }
+        cp_async_wait<0>();  // no prefetch outstanding at exit
         // termination markers: one per epilogue group (each group waits on
         // its own batch sequence); consumers and gatherers stop at the first
         for (int e = 0; e < kWsEpiGroups; ++e) {
