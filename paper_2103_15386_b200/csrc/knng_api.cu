@@ -15,6 +15,7 @@
 #include "eval_kernels.cuh"
 #include "ggm_kernels.cuh"
 #include "join_kernel.cuh"
+#include "join_ls.cuh"
 #include "join_ws.cuh"
 
 using namespace knng;
@@ -332,7 +333,8 @@ struct Run {
         const uintptr_t base = metric == KNNG_COSINE ? reinterpret_cast<uintptr_t>(Xn) : reinterpret_cast<uintptr_t>(X);
         const int al = ((static_cast<size_t>(D.d) * esz) % 16 == 0 && base % 16 == 0) ? 1 : 0;
         constexpr int NB = kJoinNodes;
-        const bool force_v3 = g_opt_join_kernel.load() == 1;
+        const int jk = g_opt_join_kernel.load();
+        const bool force_v3 = jk == 1;
         static const int dbg_mode = [] {
             const char* e = getenv("KNNG_JOIN_DBG");
             const int v = e ? atoi(e) : 0;
@@ -340,6 +342,17 @@ struct Run {
             return v;
         }();
         (void)dbg_mode;
+        if (al && jk == 0 && metric == KNNG_L2SQ && dt == KNNG_U8 && D.d <= kLsRow && D.d % 16 == 0) {
+            // uint8 rows that fit one 128-B slab: lock-step pipeline, 2 CTAs/SM
+            unsigned long long* work = reinterpret_cast<unsigned long long*>(ws + L.flag + 8);
+            cudaMemsetAsync(work, 0, 8, c.stream);
+            c.launch("k_join", [&] {
+                constexpr size_t sm = LsCfg::kSmem;
+                cudaFuncSetAttribute(k_join_ls, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+                k_join_ls<<<2 * sms, kLsThreads, sm, c.stream>>>(static_cast<const uint8_t*>(X), D, G, S, boundary, work, st);
+            });
+            return true;
+        }
         if (al && !force_v3) {
             // warp-specialised pipeline (bulk row copies need 16-B aligned,
             // 16-B multiple row slabs)
@@ -828,7 +841,7 @@ knng_status knng_set_option(const char* name, int64_t value) {
         return KNNG_OK;
     }
     if (strcmp(name, "join_kernel") == 0) {
-        if (value < 0 || value > 1) return fail(KNNG_E_USAGE, "join_kernel must be 0 or 1");
+        if (value < 0 || value > 2) return fail(KNNG_E_USAGE, "join_kernel must be 0, 1 or 2");
         g_opt_join_kernel.store(static_cast<int>(value));
         return KNNG_OK;
     }

@@ -201,6 +201,33 @@ def test_exact_u8_path_is_bit_identical_to_the_float_path(K):
         K.knng_set_option("exact_u8", 1)
 
 
+@pytest.mark.parametrize("jk", [0, 1, 2])
+@pytest.mark.parametrize("d", [128, 64])
+def test_join_kernels_u8_match(K, jk, d):
+    """Every join kernel (auto = lock-step for these uint8 rows, legacy,
+    warp-specialised) gives the oracle's graph bit for bit, including a
+    restricted (merge) run."""
+    X = datagen.make("sift", 5000, seed=8, dtype="u8", d=d)
+    assert X.dtype == np.uint8 and X.shape == (5000, d)
+    oi, od = orc.build(X, 16, 8, 5, 3)
+    nA = 2300
+    ia, da = orc.build(X[:nA], 16, 8, 3, 4)
+    ib, db = orc.build(X[nA:], 16, 8, 3, 5)
+    keys_in = np.concatenate([orc.key(da, ia), orc.key(db, ib.astype(np.uint64) + np.uint64(nA))])
+    expect = orc.merge(X, keys_in, nA, 16, 8, 3, 6, level=1)
+    try:
+        K.knng_set_option("join_kernel", jk)
+        gi, gd = K.knng_build(dev(X), 16, 5, 8, 3)
+        assert np.array_equal(gi.cpu().numpy().view(np.uint32), oi)
+        assert np.array_equal(gd.cpu().numpy(), od)
+        mi, md = K.knng_merge(dev(X[:nA]), dev(ia.view(np.int32)), dev(da), dev(X[nA:]), dev(ib.view(np.int32)),
+                              dev(db), 16, 3, 8, seed=6, level=1)
+        assert np.array_equal(mi.cpu().numpy().view(np.uint32), orc.key_ids(expect))
+        assert np.array_equal(md.cpu().numpy(), orc.key_dists(expect))
+    finally:
+        K.knng_set_option("join_kernel", 0)
+
+
 def test_legacy_join_kernel_matches(K):
     X = datagen.make("c1", 3000, seed=4)
     oi, od = orc.build(X, 10, 8, 6, 2)
