@@ -179,11 +179,14 @@ knng_status knng_debug_philox(const uint32_t* ctr, int64_t m, uint64_t seed,
  *                  then the same exact integer the canonical fp32 evaluation
  *                  (D5) yields, so the graph is bit-identical; SIFT-like data
  *                  qualifies.  0: always use the float path.
- *   "join_kernel"  0 (default): automatic -- the lock-step join
- *                  (join_ls.cuh) for uint8 L2 rows of d <= 128, d % 16 == 0,
- *                  else the warp-specialised join (join_ws.cuh);
+ *   "join_kernel"  0 (default): automatic -- the tensor-core join
+ *                  (join_tc.cuh, exact int8 Gram tiles) for uint8 L2 rows
+ *                  of d <= 128, d % 16 == 0, else the warp-specialised join
+ *                  (join_ws.cuh);
  *                  1: the batched cp.async join (join_kernel.cuh);
- *                  2: always the warp-specialised join.
+ *                  2: always the warp-specialised join;
+ *                  3: the lock-step ALU join (join_ls.cuh) where the
+ *                     tensor-core join would run.
  *                  All produce bit-identical graphs.
  *   "last_exact_u8" (read-only) 1 if the last build/merge on this thread ran
  *                  on the exact integer path.

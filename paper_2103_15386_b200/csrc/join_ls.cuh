@@ -86,6 +86,7 @@ k_join_ls(const uint8_t* __restrict__ X, Dims D, Graph G, Samples S, int64_t bou
     unsigned long long claimed = 0;
     int my_m = 0, my_q = 0, my_nb = 0, my_sl = 0;
     bool more = true;
+    bool fetch_last = false;  // the newest cp.async group is a chunk prefetch
     unsigned long long n_joins = 0, n_m = 0, n_q = 0;
     auto claim = [&]() -> unsigned long long {
         unsigned long long c0 = 0;
@@ -102,6 +103,22 @@ k_join_ls(const uint8_t* __restrict__ X, Dims D, Graph G, Samples S, int64_t bou
                              : "memory");
             }
             uint32_t* cids = cc_ids + static_cast<size_t>(buf) * 32 * 2 * cap;
+            if ((cap & 3) == 0) {  // rows of 16-B multiples: lane = node, 16-B copies
+                if (static_cast<int>(lane) < nodes) {
+                    const uint32_t* gn = S.G + static_cast<size_t>(xb + lane) * cap;
+                    const uint32_t* go = gn + static_cast<size_t>(D.n) * cap;
+                    const uint32_t dn = smem_u32(cids + lane * 2 * cap), dq = dn + 4 * cap;
+                    for (int c = 0; c < cap; c += 4) {
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dn + 4 * c), "l"(gn + c)
+                                     : "memory");
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dq + 4 * c), "l"(go + c)
+                                     : "memory");
+                    }
+                }
+                cp_async_commit();
+                fetch_last = true;
+                return;
+            }
             for (int e = lane; e < nodes * 2 * cap; e += 32) {
                 const int node = e / (2 * cap), w = e - node * 2 * cap;
                 const uint32_t* src = w < cap ? S.G + static_cast<size_t>(xb + node) * cap + w
@@ -112,11 +129,15 @@ k_join_ls(const uint8_t* __restrict__ X, Dims D, Graph G, Samples S, int64_t bou
             }
         }
         cp_async_commit();
+        fetch_last = true;
     };
     // move to the prefetched chunk; false when the work is exhausted
     auto advance = [&]() -> bool {
         if (xnext >= D.n) return false;
-        cp_async_wait<0>();
+        // the chunk's prefetch group is complete once at most the newest
+        // group (a row gather issued after it) is pending
+        if (fetch_last) cp_async_wait<0>();
+        else cp_async_wait<1>();
         __syncwarp();
         cbuf ^= 1;
         x0 = xnext;
@@ -210,6 +231,7 @@ k_join_ls(const uint8_t* __restrict__ X, Dims D, Graph G, Samples S, int64_t bou
             }
         }
         cp_async_commit();
+        fetch_last = false;
     };
 
     // --------------------------------------------------------------- filing
@@ -367,8 +389,6 @@ k_join_ls(const uint8_t* __restrict__ X, Dims D, Graph G, Samples S, int64_t bou
         // ---- GetNearestObject per output key (Alg. 2): output o is key j of
         // node i (obase[i] <= o): c_nn(u_j) (j < m), c_no(u_{j-m}) (j < 2m),
         // c_on(w_{j-2m}); the min over the partials of the blocks covering it
-        const unsigned long long* rowp = parts;
-        const unsigned long long* colp = parts + 4 * kLsBlocks;
         const int total = P.nout;
 #pragma unroll
         for (int r = 0; r < kLsKeys; ++r) {
@@ -382,29 +402,40 @@ k_join_ls(const uint8_t* __restrict__ X, Dims D, Graph G, Samples S, int64_t bou
                 const int mi = P.m[i], qi = P.q[i];
                 const int mgi = (mi + 3) >> 2, qgi = (qi + 3) >> 2, bb = P.bbase[i];
                 const int nnn_i = mgi * (mgi + 1) / 2;
-                if (j < 2 * mi) {
-                    const int u = j < mi ? j : j - mi, Iu = u >> 2, rr = u & 3;
-                    if (j < mi) {  // as a row of blocks (I, J <= I) and a column of (I' >= I, I)
-                        for (int Jb = 0; Jb <= Iu; ++Jb) {
-                            const uint64_t tv = rowp[(bb + Iu * (Iu + 1) / 2 + Jb) * 4 + rr];
-                            v = tv < v ? tv : v;
-                        }
-                        for (int I2 = Iu; I2 < mgi; ++I2) {
-                            const uint64_t tv = colp[(bb + I2 * (I2 + 1) / 2 + Iu) * 4 + rr];
-                            v = tv < v ? tv : v;
-                        }
-                    } else {  // rows of the NEW-OLD blocks (I, J)
-                        for (int Jb = 0; Jb < qgi; ++Jb) {
-                            const uint64_t tv = rowp[(bb + nnn_i + Iu * qgi + Jb) * 4 + rr];
-                            v = tv < v ? tv : v;
-                        }
+                // the partials covering the key form one or two strided runs
+                // (in u64 units): run A of na entries from a0 step sa, then
+                // (c_nn only) run B from b0 with a step growing by 4 each time
+                int na, a0, sa, nb = 0, b0 = 0, sb0 = 0;
+                if (j < mi) {  // c_nn(u): row of blocks (I, J <= I), column of (I' >= I, I)
+                    const int Iu = j >> 2, rr = j & 3;
+                    na = Iu + 1;
+                    a0 = (bb + Iu * (Iu + 1) / 2) * 4 + rr;
+                    sa = 4;
+                    nb = mgi - Iu;
+                    b0 = 4 * kLsBlocks + (bb + Iu * (Iu + 1) / 2 + Iu) * 4 + rr;
+                    sb0 = 4 * (Iu + 1);
+                } else if (j < 2 * mi) {  // c_no(u): rows of the NEW-OLD blocks (I, J)
+                    const int u = j - mi, Iu = u >> 2, rr = u & 3;
+                    na = qgi;
+                    a0 = (bb + nnn_i + Iu * qgi) * 4 + rr;
+                    sa = 4;
+                } else {  // c_on(w): columns of the NEW-OLD blocks (I, J_w)
+                    const int oo = j - 2 * mi;
+                    na = mgi;
+                    a0 = 4 * kLsBlocks + (bb + nnn_i + (oo >> 2)) * 4 + (oo & 3);
+                    sa = 4 * qgi;
+                }
+                const int ntot = na + nb;
+                int addr = a0, step = sa;
+                for (int t = 0; t < ntot; ++t) {
+                    if (t == na) {
+                        addr = b0;
+                        step = sb0;
                     }
-                } else {  // columns of the NEW-OLD blocks (I, J_w)
-                    const int oo = j - 2 * mi, Jw = oo >> 2, c = oo & 3;
-                    for (int Ib = 0; Ib < mgi; ++Ib) {
-                        const uint64_t tv = colp[(bb + nnn_i + Ib * qgi + Jw) * 4 + c];
-                        v = tv < v ? tv : v;
-                    }
+                    const uint64_t tv = parts[addr];
+                    v = tv < v ? tv : v;
+                    addr += step;
+                    if (t >= na) step += 4;
                 }
                 // target: the NEW sample u_j (c_nn, c_no) or the OLD sample w_j (c_on)
                 const int sbi = P.sbase[i], mpi = (mi + 3) & ~3;

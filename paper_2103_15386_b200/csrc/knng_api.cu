@@ -16,6 +16,7 @@
 #include "ggm_kernels.cuh"
 #include "join_kernel.cuh"
 #include "join_ls.cuh"
+#include "join_tc.cuh"
 #include "join_ws.cuh"
 
 using namespace knng;
@@ -47,7 +48,7 @@ constexpr int kMaxIters = 256;
 // ---------------------------------------------------------------- layout
 struct Layout {
     size_t keys, newmask, kth, bcnt, bucket, fwd, fcnt, rcnt, rcur, off, rsrc, G, gcnt, bsum, cand, stats,
-        xnorm, xu8, reserved, flag, total;
+        xnorm, xu8, sqn, reserved, flag, total;
 };
 
 int64_t scan_blocks(int64_t n) { return (n + kScanBlock - 1) / kScanBlock; }
@@ -83,6 +84,7 @@ Layout make_layout(int64_t n, int d, int k, int p, bool cosine, bool own_keys, b
     L.xnorm = cosine ? take(static_cast<size_t>(n) * d * 4) : 0;
     L.reserved = merge ? take(static_cast<size_t>(n) * (k / 2 > 0 ? k / 2 : 1) * 8) : 0;
     L.xu8 = u8copy ? take(static_cast<size_t>(n) * d) : 0;  // exact integer copy (option exact_u8)
+    L.sqn = take(static_cast<size_t>(n) * 4);                // exact squared norms (uint8 tensor-core join)
     L.flag = take(16);
     L.total = off;
     return L;
@@ -193,6 +195,7 @@ struct Run {
     const float* Xn;
     uint64_t seed;
     int64_t boundary = -1;
+    bool sqn_ready = false;  // L.sqn holds the exact squared norms of X
 
     Run(Ctx& ctx) : c(ctx) {}
 
@@ -342,7 +345,28 @@ struct Run {
             return v;
         }();
         (void)dbg_mode;
-        if (al && jk == 0 && metric == KNNG_L2SQ && dt == KNNG_U8 && D.d <= kLsRow && D.d % 16 == 0) {
+        const bool u8_slab = al && metric == KNNG_L2SQ && dt == KNNG_U8 && D.d <= kLsRow && D.d % 16 == 0;
+        if (u8_slab && jk == 0) {
+            // uint8 rows of one 128-B slab: Gram tiles on the tensor cores
+            int* sqn = reinterpret_cast<int*>(ws + L.sqn);
+            if (!sqn_ready) {
+                c.launch("k_sqnorm_u8", [&] {
+                    k_sqnorm_u8<<<static_cast<int>((D.n + 255) / 256), 256, 0, c.stream>>>(
+                        static_cast<const uint8_t*>(X), D.n, D.d, sqn);
+                });
+                sqn_ready = true;
+            }
+            unsigned long long* work = reinterpret_cast<unsigned long long*>(ws + L.flag + 8);
+            cudaMemsetAsync(work, 0, 8, c.stream);
+            c.launch("k_join", [&] {
+                constexpr size_t sm = TcCfg::kSmem;
+                cudaFuncSetAttribute(k_join_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+                k_join_tc<<<kTcCtasPerSm * sms, kTcThreads, sm, c.stream>>>(static_cast<const uint8_t*>(X), sqn, D, G,
+                                                                           S, boundary, work, st);
+            });
+            return true;
+        }
+        if (u8_slab && jk == 3) {
             // uint8 rows that fit one 128-B slab: lock-step pipeline, 2 CTAs/SM
             unsigned long long* work = reinterpret_cast<unsigned long long*>(ws + L.flag + 8);
             cudaMemsetAsync(work, 0, 8, c.stream);
@@ -841,7 +865,7 @@ knng_status knng_set_option(const char* name, int64_t value) {
         return KNNG_OK;
     }
     if (strcmp(name, "join_kernel") == 0) {
-        if (value < 0 || value > 2) return fail(KNNG_E_USAGE, "join_kernel must be 0, 1 or 2");
+        if (value < 0 || value > 3) return fail(KNNG_E_USAGE, "join_kernel must be 0, 1, 2 or 3");
         g_opt_join_kernel.store(static_cast<int>(value));
         return KNNG_OK;
     }
