@@ -14,7 +14,7 @@
 // into the 128 rows; only the diagonal blocks of the Gram matrix are used.
 //
 // Thread s of the 4 epilogue warps owns TMEM lane s = sample slot s and scans
-// its own node's columns (tcgen05.ld, 32 columns at a time):
+// its own node's columns (tcgen05.ld, 16 columns at a time):
 //   NEW sample u: c_nn(u) = min over the other NEW samples, c_no(u) = min
 //                 over the OLD samples;
 //   OLD sample w: c_on(w) = min over the NEW samples
@@ -91,14 +91,12 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+__device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t (&r)[16]) {
     asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%16];"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
         : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -254,18 +252,23 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
     int nv_next = 0;  // this thread's staged n'_c of the next batch
     uint32_t side_next = 0;
     auto gather = [&](const TcPlan& P, uint8_t* dst) {
-        if (part < kchunks) {
+        const int nslots = P.nslots;  // hoisted: the asm below clobbers memory
+        const uint32_t dbase = smem_u32(dst);
+        if (part < nchunks) {
             const uint8_t* src0 = X + part * 16;
-            for (int slot = row0; slot < P.nslots; slot += 16) {
+            for (int slot = row0; slot < nslots; slot += 16) {
                 const uint32_t id = P.ids[slot];
-                const uint32_t s = smem_u32(dst + slot * 128 + ((part ^ (slot & 7)) << 4));
-                if (part < nchunks)
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s),
-                                 "l"(src0 + static_cast<size_t>(id) * d)
-                                 : "memory");
-                else
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, 0;\n" ::"r"(s), "l"(X) : "memory");
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
+                                 dbase + slot * 128 + ((part ^ (slot & 7)) << 4)),
+                             "l"(src0 + static_cast<size_t>(id) * d)
+                             : "memory");
             }
+        } else if (part < kchunks) {
+            for (int slot = row0; slot < nslots; slot += 16)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, 0;\n" ::"r"(
+                                 dbase + slot * 128 + ((part ^ (slot & 7)) << 4)),
+                             "l"(X)
+                             : "memory");
         }
         cp_async_commit();
         // squared norm of slot tid's row (exact integer), staged as n * 128 + slot
@@ -275,36 +278,36 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
     };
 
     // --------------------------------------------------------------- filing
-    uint64_t f1_key[2], f1_th[2], f1_bo[2];
-    uint32_t f1_tgt[2];
-    uint64_t f2_key[2], f2_bo[2];
-    uint32_t f2_sl[2];
+    // stage 1 (batch b): the row's 2 keys, its target (the row's sample) and
+    // the target's k-th key / bucket offset loads; stage 2 (b+1): atomicAdd
+    // slots; stage 3 (b+2): stores
+    uint64_t f1_key[2], f1_th = 0, f1_bo = 0;
+    uint32_t f1_tgt = 0;
+    uint64_t f2_key[2], f2_pos[2];
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
         f1_key[r] = kSentinel;
-        f1_th[r] = 0;
-        f1_bo[r] = 0;
-        f1_tgt[r] = 0;
         f2_key[r] = kSentinel;
-        f2_bo[r] = 0;
-        f2_sl[r] = 0xFFFFFFFFu;
+        f2_pos[r] = 0;
     }
     unsigned long long n_cand = 0, n_app = 0, my_pairs = 0;
     auto file_store = [&]() {
 #pragma unroll
         for (int r = 0; r < 2; ++r)
-            if (f2_sl[r] != 0xFFFFFFFFu) G.bucket[f2_bo[r] + f2_sl[r]] = f2_key[r];
+            if (f2_key[r] != kSentinel) G.bucket[f2_pos[r]] = f2_key[r];
     };
     auto file_atomic = [&]() {
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            const bool ok = f1_key[r] != kSentinel && f1_key[r] < f1_th[r];  // D17
-            n_app += ok;
-            f2_sl[r] = ok ? atomicAdd(G.bcnt + f1_tgt[r], 1u) : 0xFFFFFFFFu;
-            f2_key[r] = f1_key[r];
-            f2_bo[r] = f1_bo[r];
-            f1_key[r] = kSentinel;
-        }
+        const bool ok0 = f1_key[0] < f1_th, ok1 = f1_key[1] < f1_th;  // D17 (the sentinel never passes)
+        n_app += ok0 + ok1;
+        uint32_t sl = 0;
+        if (ok0 || ok1) sl = atomicAdd(G.bcnt + f1_tgt, static_cast<uint32_t>(ok0 + ok1));
+        f2_key[0] = ok0 ? f1_key[0] : kSentinel;
+        f2_pos[0] = f1_bo + sl;
+        f2_key[1] = ok1 ? f1_key[1] : kSentinel;
+        f2_pos[1] = f1_bo + sl + (ok0 ? 1 : 0);
+        f1_key[0] = kSentinel;
+        f1_key[1] = kSentinel;
+        f1_th = 0;
     };
 
     // ------------------------------------------------------------- prologue
@@ -386,23 +389,26 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
         int minA = INT_MAX, minB = INT_MAX;
         mbar_wait(mma_bar, b & 1);
         tc_fence_after();
-        for (int ch = wlo >> 5; ch * 32 < whi; ++ch) {
-            uint32_t r[32];
-            tc_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + ch * 32, r);
-            const int cb = ch * 32;
+        // 16-column chunks over the warp's column range (the union of its
+        // rows' node ranges)
+        for (int cb = wlo & ~15; cb < whi; cb += 16) {
+            uint32_t r[16];
+            tc_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + cb, r);
             uint32_t A = act ? bit_range(sb - cb, sb + m - cb) : 0u;
-            if (isNEW && s >= cb && s < cb + 32) A &= ~(1u << (s - cb));
+            if (isNEW && s >= cb && s < cb + 16) A &= ~(1u << (s - cb));
             uint32_t B = isNEW ? bit_range(sb + m - cb, sb + m + q - cb) : 0u;
             if (restricted) {
-                const uint32_t sd = side[buf * 4 + ch];
+                const uint32_t sd = side[buf * 4 + (cb >> 5)] >> (cb & 16);
                 const uint32_t allow = myside ? ~sd : sd;
                 A &= allow;
                 B &= allow;
             }
+            A &= 0xFFFFu;
+            B &= 0xFFFFu;
             if (isNEW) my_pairs += __popc(A & bit_range(0, s - cb)) + __popc(B);
             const int4* nv4 = reinterpret_cast<const int4*>(nb + cb);
 #pragma unroll
-            for (int g = 0; g < 8; ++g) {
+            for (int g = 0; g < 4; ++g) {
                 const int4 n4 = nv4[g];
                 const int kk[4] = {n4.x - static_cast<int>(r[4 * g] << 8), n4.y - static_cast<int>(r[4 * g + 1] << 8),
                                    n4.z - static_cast<int>(r[4 * g + 2] << 8),
@@ -427,16 +433,11 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
             k2 = make_key(static_cast<float>(ns + (minB >> 7)), P.ids[minB & 127]);
         f1_key[0] = k1;
         f1_key[1] = k2;
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            f1_tgt[r] = my_id;
-            f1_th[r] = 0;
-            f1_bo[r] = 0;
-            if (f1_key[r] != kSentinel) {  // D15: (inf, inf) inserts nothing
-                ++n_cand;
-                f1_th[r] = __ldg(G.kth + my_id);
-                f1_bo[r] = __ldg(G.boff + my_id);
-            }
+        f1_tgt = my_id;
+        n_cand += (k1 != kSentinel) + (k2 != kSentinel);
+        if (k1 != kSentinel || k2 != kSentinel) {  // D15: (inf, inf) inserts nothing
+            f1_th = __ldg(G.kth + my_id);
+            f1_bo = __ldg(G.boff + my_id);
         }
         // stage the next batch's norms (their loads were issued with the gather)
         nrm[(buf ^ 1) * kTcRows + tid] = nv_next * 128 + tid;
@@ -477,13 +478,20 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
     }
 }
 
-// exact squared norms of uint8 rows (int32; d <= 128 keeps them < 2^23)
+// exact squared norms of uint8 rows (int32; d <= 128 keeps them < 2^23);
+// d % 16 == 0 and 16-B aligned rows (the tensor-core join's preconditions)
 __global__ void k_sqnorm_u8(const uint8_t* __restrict__ X, int64_t n, int d, int* __restrict__ out) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const uint8_t* x = X + i * d;
+    const uint4* x = reinterpret_cast<const uint4*>(X + i * d);
     unsigned int acc = 0;
-    for (int j = 0; j < d; ++j) acc += static_cast<unsigned int>(x[j]) * x[j];
+    for (int j = 0; j < d / 16; ++j) {
+        const uint4 v = __ldg(x + j);
+        acc = __dp4a(v.x, v.x, acc);
+        acc = __dp4a(v.y, v.y, acc);
+        acc = __dp4a(v.z, v.z, acc);
+        acc = __dp4a(v.w, v.w, acc);
+    }
     out[i] = static_cast<int>(acc);
 }
 
