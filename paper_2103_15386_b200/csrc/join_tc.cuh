@@ -28,12 +28,14 @@
 // With n'_c = n_c * 128 + c staged per batch, one IMAD per column forms it.
 //
 // CTA = 4 epilogue/gather warps + 1 planning warp; 4 CTAs per SM, each with
-// 128 TMEM columns.  Iteration b of a CTA:
-//     wait rows(b); proxy fence; sync
-//     thread 0: 4 MMAs (K = 128) of batch b -> TMEM, commit -> mbarrier
-//     warps 0-3: cp.async rows(b+1) (SW128 K-major layout), norm loads
-//                wait MMA(b); row scans; filing of b / b-1 / b-2 (as join_ls)
-//     warp 4: plan(b+2) from the chunk cache
+// 128 TMEM columns.  The planning warp fills a 4-deep plan ring (mbarrier
+// hand-off) from the chunk cache, running ahead of the rest.  Iteration b of
+// warps 0-3 (two row buffers, two batches of rows in flight):
+//     wait rows(b); proxy fence; named barrier
+//     thread 0: kch MMAs (K = 32 each) of batch b -> TMEM, commit -> mbarrier
+//     wait MMA(b) -> rows[b & 1] is free: cp.async rows(b+2) into it (SW128
+//       K-major layout) and load their norms
+//     row scans of b (tcgen05.ld); filing of b / b-1 / b-2 (as join_ls)
 #pragma once
 #include <climits>
 
@@ -46,6 +48,7 @@ constexpr int kTcWarps = 5;      // 4 epilogue/gather + 1 planning
 constexpr int kTcThreads = kTcWarps * 32;
 constexpr int kTcPlanWarp = 4;
 constexpr int kTcCtasPerSm = 4;  // 4 x 128 TMEM columns
+constexpr int kTcPlans = 4;      // plan ring: b (scan), b+1, b+2 (rows in flight), b+3 (being formed)
 
 struct TcPlan {
     int nnodes;  // 0 = no more work
@@ -57,14 +60,14 @@ struct TcPlan {
 
 struct TcCfg {
     static constexpr size_t kRowBytes = static_cast<size_t>(kTcRows) * 128;  // one batch, SW128 K-major
-    static constexpr size_t kNrmOff = 2 * kRowBytes;                           // int32 n'_c [2][128]
-    static constexpr size_t kSideOff = kNrmOff + 2 * kTcRows * 4;              // u32 [2][4]
-    static constexpr size_t kPlanOff = kSideOff + 2 * 4 * 4;
-    static constexpr size_t kCacheOff = (kPlanOff + 3 * sizeof(TcPlan) + 15) & ~size_t(15);
+    static constexpr size_t kNrmOff = 2 * kRowBytes;                           // int32 n'_c [3][128]
+    static constexpr size_t kSideOff = kNrmOff + 3 * kTcRows * 4;              // u32 [3][4]
+    static constexpr size_t kPlanOff = kSideOff + 3 * 4 * 4;
+    static constexpr size_t kCacheOff = (kPlanOff + kTcPlans * sizeof(TcPlan) + 15) & ~size_t(15);
     static constexpr size_t kCacheCnt = 2 * 64;
     static constexpr size_t kCacheBytes = kCacheCnt + 2 * 32 * 2 * 32 * sizeof(uint32_t);
     static constexpr size_t kBarOff = (kCacheOff + kCacheBytes + 7) & ~size_t(7);
-    static constexpr size_t kUsed = kBarOff + 16;  // mbarrier + TMEM address
+    static constexpr size_t kUsed = kBarOff + 8 * (1 + 2 * kTcPlans) + 8;  // mbarriers + TMEM address
     static constexpr size_t kSmem = kUsed + 1024;  // + slack to align the rows to 1024 B
     static_assert(kTcCtasPerSm * (kSmem + 1024) <= 233472, "4 CTAs per SM");
 };
@@ -100,6 +103,17 @@ __device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t (&r)[16]) {
         : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+// wait with the hardware suspend hint: the waiting warp is descheduled
+// instead of polling (the planning warp is usually a full ring ahead)
+__device__ __forceinline__ void mbar_wait_suspend(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(1000000)
+        : "memory");
+}
 // bits [a, b) of a 32-bit word, clamped
 __device__ __forceinline__ uint32_t bit_range(int a, int b) {
     a = max(a, 0);
@@ -122,7 +136,9 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
     uint8_t* cc_cnt = tc_smem + TcCfg::kCacheOff;
     uint32_t* cc_ids = reinterpret_cast<uint32_t*>(tc_smem + TcCfg::kCacheOff + TcCfg::kCacheCnt);
     uint64_t* mma_bar = reinterpret_cast<uint64_t*>(tc_smem + TcCfg::kBarOff);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tc_smem + TcCfg::kBarOff + 8);
+    uint64_t* plan_full = mma_bar + 1;             // [kTcPlans] planning warp -> warps 0-3
+    uint64_t* plan_empty = plan_full + kTcPlans;   // [kTcPlans] warps 0-3 -> planning warp
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(plan_empty + kTcPlans);
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -249,8 +265,8 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
     // the SW128 layout; chunks in [d/16, 2 kch) are zero-filled
     const int part = tid & 7, row0 = tid >> 3;
     const int nchunks = d >> 4, kchunks = 2 * kch;
-    int nv_next = 0;  // this thread's staged n'_c of the next batch
-    uint32_t side_next = 0;
+    int nv_next = 0, nv_prev = 0;  // this thread's slot norm of batches b+2 and b+1
+    uint32_t side_next = 0, side_prev = 0;
     auto gather = [&](const TcPlan& P, uint8_t* dst) {
         const int nslots = P.nslots;  // hoisted: the asm below clobbers memory
         const uint32_t dbase = smem_u32(dst);
@@ -319,129 +335,164 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
     }
     if (tid == 0) {
         mbar_init(mma_bar, 1);
+        for (int i = 0; i < kTcPlans; ++i) {
+            mbar_init(plan_full + i, 1);
+            mbar_init(plan_empty + i, kTcPlanWarp);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == kTcPlanWarp) {
-        xnext = static_cast<int64_t>(__shfl_sync(kFull, claim(), 0));
-        claimed = claim();
-        fetch(0, xnext);
-        form_plan(plans[0]);
-        form_plan(plans[1]);
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    if (warp < kTcPlanWarp && plans[0].nnodes > 0) {
-        gather(plans[0], rows);
-        nrm[tid] = nv_next * 128 + tid;
-        if (lane == 0) side[warp] = side_next;
-    }
 
-    for (uint32_t b = 0;; ++b) {
-        const TcPlan& P = plans[b % 3];
-        const int buf = b & 1;
-        if (warp < kTcPlanWarp) {
-            cp_async_wait<0>();
+    if (warp == kTcPlanWarp) {
+        // ---- planning warp: runs up to kTcPlans batches ahead
+        xnext = static_cast<int64_t>(__shfl_sync(kFull, claim(), 0));
+        claimed = claim();
+        fetch(0, xnext);
+        for (uint32_t t = 0;; ++t) {
+            const int slot = t % kTcPlans;
+            if (t >= kTcPlans) mbar_wait_suspend(plan_empty + slot, ((t / kTcPlans) - 1) & 1);
+            form_plan(plans[slot]);
+            const bool last = plans[slot].nnodes == 0;
+            if (lane == 0) mbar_arrive(plan_full + slot);
+            if (last) break;
+        }
+    } else {
+        // ---- warps 0-3: two batches of rows in flight
+        bool ended = false;  // a terminator plan has been seen
+        for (int t = 0; t < 2; ++t) {
+            if (!ended) {
+                mbar_wait(plan_full + t, 0);
+                ended = plans[t].nnodes == 0;
+            }
+            if (!ended) {
+                gather(plans[t], rows + t * TcCfg::kRowBytes);
+            } else {
+                cp_async_commit();
+            }
+            if (t == 0) {
+                nrm[tid] = nv_next * 128 + tid;
+                if (lane == 0) side[warp] = side_next;
+            } else {
+                nv_prev = nv_next;
+                side_prev = side_next;
+            }
+        }
+        for (uint32_t b = 0;; ++b) {
+            const int slot = b % kTcPlans;
+            const TcPlan& P = plans[slot];
+            const int buf = b & 1;
+            if (P.nnodes == 0) break;  // waited for at b - 2 (or in the prologue)
+            cp_async_wait<1>();        // rows(b); rows(b+1) may be in flight
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // cp.async data -> MMA operand reads
-        }
-        __syncthreads();  // rows(b), n'(b), plan(b+1) visible; TMEM free
-        if (P.nnodes == 0) break;
-        if (tid == 0) {
+            named_bar(1, kTcPlanWarp * 32);  // rows(b), n'(b) visible; TMEM reads of b-1 done
+            if (tid == 0) {
+                tc_fence_after();
+                const uint32_t base = smem_u32(rows + buf * TcCfg::kRowBytes);
+                for (int k = 0; k < kch; ++k) {
+                    const uint64_t desc = tc_smem_desc(base + 32 * k);
+                    tc_mma_i8(tmem, desc, desc, k > 0 ? 1u : 0u);
+                }
+                tc_commit(mma_bar);
+            }
+
+            // ---- my row of batch b
+            const int s = tid;
+            const int nd = P.map[s];
+            bool isNEW = false, isOLD = false;
+            int sb = 0, m = 0, q = 0;
+            if (nd != 0xFF) {
+                sb = P.sb[nd];
+                m = P.m[nd];
+                q = P.q[nd];
+                isNEW = s - sb < m;
+                isOLD = !isNEW;
+            }
+            const bool act = isNEW || isOLD;
+            const int lo = act ? sb : kTcRows;
+            const int hi = act ? (isNEW ? sb + m + q : sb + m) : 0;
+            const int wlo = __reduce_min_sync(kFull, lo), whi = __reduce_max_sync(kFull, hi);
+            const uint32_t my_id = P.ids[s];
+            const bool myside = restricted && static_cast<int64_t>(my_id) >= boundary;
+            const int nbuf = b % 3;  // norms/sides: b (scan), b+1, b+2 (staged by other warps meanwhile)
+            const int* nb = nrm + nbuf * kTcRows;
+            const int ns = nb[s] >> 7;  // n_s
+            int minA = INT_MAX, minB = INT_MAX;
+            mbar_wait(mma_bar, b & 1);
             tc_fence_after();
-            const uint32_t base = smem_u32(rows + buf * TcCfg::kRowBytes);
-            for (int k = 0; k < kch; ++k) {
-                const uint64_t desc = tc_smem_desc(base + 32 * k);
-                tc_mma_i8(tmem, desc, desc, k > 0 ? 1u : 0u);
-            }
-            tc_commit(mma_bar);
-        }
-        if (warp == kTcPlanWarp) {
-            form_plan(plans[(b + 2) % 3]);
-            continue;
-        }
 
-        // ---- warps 0-3: next batch's rows while the MMA runs
-        {
-            const TcPlan& Pn = plans[(b + 1) % 3];
-            if (Pn.nnodes > 0) gather(Pn, rows + (buf ^ 1) * TcCfg::kRowBytes);
-        }
-
-        // ---- row scans of batch b
-        const int s = tid;
-        const int nd = P.map[s];
-        bool isNEW = false, isOLD = false;
-        int sb = 0, m = 0, q = 0;
-        if (nd != 0xFF) {
-            sb = P.sb[nd];
-            m = P.m[nd];
-            q = P.q[nd];
-            isNEW = s - sb < m;
-            isOLD = !isNEW;
-        }
-        const bool act = isNEW || isOLD;
-        const int lo = act ? sb : kTcRows;
-        const int hi = act ? (isNEW ? sb + m + q : sb + m) : 0;
-        const int wlo = __reduce_min_sync(kFull, lo), whi = __reduce_max_sync(kFull, hi);
-        const uint32_t my_id = P.ids[s];
-        const bool myside = restricted && static_cast<int64_t>(my_id) >= boundary;
-        const int* nb = nrm + buf * kTcRows;
-        int minA = INT_MAX, minB = INT_MAX;
-        mbar_wait(mma_bar, b & 1);
-        tc_fence_after();
-        // 16-column chunks over the warp's column range (the union of its
-        // rows' node ranges)
-        for (int cb = wlo & ~15; cb < whi; cb += 16) {
-            uint32_t r[16];
-            tc_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + cb, r);
-            uint32_t A = act ? bit_range(sb - cb, sb + m - cb) : 0u;
-            if (isNEW && s >= cb && s < cb + 16) A &= ~(1u << (s - cb));
-            uint32_t B = isNEW ? bit_range(sb + m - cb, sb + m + q - cb) : 0u;
-            if (restricted) {
-                const uint32_t sd = side[buf * 4 + (cb >> 5)] >> (cb & 16);
-                const uint32_t allow = myside ? ~sd : sd;
-                A &= allow;
-                B &= allow;
+            // ---- MMA(b) has read rows[buf]: gather batch b+2 into it
+            if (!ended) {
+                const int s2 = (b + 2) % kTcPlans;
+                mbar_wait(plan_full + s2, ((b + 2) / kTcPlans) & 1);
+                ended = plans[s2].nnodes == 0;
             }
-            A &= 0xFFFFu;
-            B &= 0xFFFFu;
-            if (isNEW) my_pairs += __popc(A & bit_range(0, s - cb)) + __popc(B);
-            const int4* nv4 = reinterpret_cast<const int4*>(nb + cb);
+            if (!ended) gather(plans[(b + 2) % kTcPlans], rows + buf * TcCfg::kRowBytes);
+            else cp_async_commit();
+
+            // 16-column chunks over the warp's column range (the union of its
+            // rows' node ranges)
+            for (int cb = wlo & ~15; cb < whi; cb += 16) {
+                uint32_t r[16];
+                tc_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + cb, r);
+                uint32_t A = act ? bit_range(sb - cb, sb + m - cb) : 0u;
+                if (isNEW && s >= cb && s < cb + 16) A &= ~(1u << (s - cb));
+                uint32_t B = isNEW ? bit_range(sb + m - cb, sb + m + q - cb) : 0u;
+                if (restricted) {
+                    const uint32_t sd = side[nbuf * 4 + (cb >> 5)] >> (cb & 16);
+                    const uint32_t allow = myside ? ~sd : sd;
+                    A &= allow;
+                    B &= allow;
+                }
+                A &= 0xFFFFu;
+                B &= 0xFFFFu;
+                if (isNEW) my_pairs += __popc(A & bit_range(0, s - cb)) + __popc(B);
+                const int4* nv4 = reinterpret_cast<const int4*>(nb + cb);
 #pragma unroll
-            for (int g = 0; g < 4; ++g) {
-                const int4 n4 = nv4[g];
-                const int kk[4] = {n4.x - static_cast<int>(r[4 * g] << 8), n4.y - static_cast<int>(r[4 * g + 1] << 8),
-                                   n4.z - static_cast<int>(r[4 * g + 2] << 8),
-                                   n4.w - static_cast<int>(r[4 * g + 3] << 8)};
+                for (int g = 0; g < 4; ++g) {
+                    const int4 n4 = nv4[g];
+                    const int kk[4] = {n4.x - static_cast<int>(r[4 * g] << 8),
+                                       n4.y - static_cast<int>(r[4 * g + 1] << 8),
+                                       n4.z - static_cast<int>(r[4 * g + 2] << 8),
+                                       n4.w - static_cast<int>(r[4 * g + 3] << 8)};
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    if ((A >> (4 * g + e)) & 1u) minA = min(minA, kk[e]);
-                    if ((B >> (4 * g + e)) & 1u) minB = min(minB, kk[e]);
+                    for (int e = 0; e < 4; ++e) {
+                        if ((A >> (4 * g + e)) & 1u) minA = min(minA, kk[e]);
+                        if ((B >> (4 * g + e)) & 1u) minB = min(minB, kk[e]);
+                    }
                 }
             }
-        }
-        tc_fence_before();
+            tc_fence_before();
 
-        // ---- deferred filing of the two previous batches, then this one's keys
-        file_store();
-        file_atomic();
-        const int ns = nb[s] >> 7;  // n_s
-        uint64_t k1 = kSentinel, k2 = kSentinel;
-        if (act && minA != INT_MAX)
-            k1 = make_key(static_cast<float>(ns + (minA >> 7)), P.ids[minA & 127]);
-        if (isNEW && minB != INT_MAX)
-            k2 = make_key(static_cast<float>(ns + (minB >> 7)), P.ids[minB & 127]);
-        f1_key[0] = k1;
-        f1_key[1] = k2;
-        f1_tgt = my_id;
-        n_cand += (k1 != kSentinel) + (k2 != kSentinel);
-        if (k1 != kSentinel || k2 != kSentinel) {  // D15: (inf, inf) inserts nothing
-            f1_th = __ldg(G.kth + my_id);
-            f1_bo = __ldg(G.boff + my_id);
+            // ---- deferred filing of the two previous batches, then this one's keys
+            file_store();
+            file_atomic();
+            uint64_t k1 = kSentinel, k2 = kSentinel;
+            if (act && minA != INT_MAX)
+                k1 = make_key(static_cast<float>(ns + (minA >> 7)), P.ids[minA & 127]);
+            if (isNEW && minB != INT_MAX)
+                k2 = make_key(static_cast<float>(ns + (minB >> 7)), P.ids[minB & 127]);
+            f1_key[0] = k1;
+            f1_key[1] = k2;
+            f1_tgt = my_id;
+            n_cand += (k1 != kSentinel) + (k2 != kSentinel);
+            if (k1 != kSentinel || k2 != kSentinel) {  // D15: (inf, inf) inserts nothing
+                f1_th = __ldg(G.kth + my_id);
+                f1_bo = __ldg(G.boff + my_id);
+            }
+            // batch b+1's norms (their loads were issued one iteration ago);
+            // buffer (b+1) % 3 was last read by the scans of b-2
+            __syncwarp();
+            nrm[((b + 1) % 3) * kTcRows + tid] = nv_prev * 128 + tid;
+            nv_prev = nv_next;
+            if (lane == 0) {
+                side[((b + 1) % 3) * 4 + warp] = side_prev;
+                mbar_arrive(plan_empty + slot);  // this warp is done with plan b
+            }
+            side_prev = side_next;
         }
-        // stage the next batch's norms (their loads were issued with the gather)
-        nrm[(buf ^ 1) * kTcRows + tid] = nv_next * 128 + tid;
-        if (lane == 0) side[(buf ^ 1) * 4 + warp] = side_next;
     }
     if (warp < kTcPlanWarp) {
         file_store();
