@@ -28,11 +28,20 @@ __all__ = ["gmm", "make", "SHAPES", "sample_nodes"]
 
 
 def gmm(n: int, d: int, C: int, r: int, sigma_c: float, sigma_a: float,
-        sigma_n: float, seed: int, chunk: int = 1 << 18) -> np.ndarray:
-    """float64 GMM-LR rows [n, d] (see module docstring)."""
+        sigma_n: float, seed: int, chunk: int = 1 << 18,
+        part: int | None = None) -> np.ndarray:
+    """float64 GMM-LR rows [n, d] (see module docstring).
+
+    part: None -> rows drawn from the same stream as the mixture (the
+    single-set recipe).  An int -> the mixture (mu, A) still comes from
+    `seed`, the rows from the independent stream (seed, part): shard `part`
+    of one global dataset, so shards built on different GPUs share the
+    components (the sharded build's weak-scaling workload)."""
     rng = np.random.default_rng(seed)
     mu = rng.standard_normal((C, d)) * sigma_c
     At = rng.standard_normal((C, r, d)) * (sigma_a / np.sqrt(r))  # A_c^T
+    if part is not None:
+        rng = np.random.default_rng([seed, 0x5EED, part])
     out = np.empty((n, d), dtype=np.float64)
     chunk = max(1, min(chunk, (1 << 26) // max(1, d)))
     for lo in range(0, n, chunk):
@@ -58,16 +67,18 @@ SHAPES = {
 
 
 def make(shape: str, n: int, seed: int = 1, dtype: str = "f32",
-         d: int | None = None) -> np.ndarray:
+         d: int | None = None, part: int | None = None,
+         components: int | None = None) -> np.ndarray:
     """Synthetic vectors of a named shape: float32 [n, d] (or uint8 for
-    shape 'sift' with dtype='u8')."""
+    shape 'sift' with dtype='u8').  part / components: shard `part` of a
+    global set whose mixture has `components` components (see gmm)."""
     if shape == "uniform":
         rng = np.random.default_rng(seed)
         return rng.random((n, d or 32), dtype=np.float64).astype(np.float32)
     dd, C, r, sc, sa, sn = SHAPES[shape]
     d = d or dd
-    C = min(C, max(1, n // 8))
-    x = gmm(n, d, C, r, sc, sa, sn, seed)
+    C = components or min(C, max(1, n // 8))
+    x = gmm(n, d, C, r, sc, sa, sn, seed, part=part)
     if shape == "sift":
         x = np.clip(np.rint(32.0 + 24.0 * x), 0.0, 255.0)
         return x.astype(np.uint8) if dtype == "u8" else x.astype(np.float32)

@@ -465,8 +465,21 @@ struct Run {
     }
 };
 
+std::atomic<bool> g_pool_ready[64];
+
 knng_status get_workspace(Ctx& c, void* workspace, size_t bytes, size_t need, char** out) {
     if (workspace == nullptr && bytes == 0) {
+        // Library-owned workspace comes from the device's default stream-
+        // ordered pool; keep freed blocks reserved in the pool (release
+        // threshold = max) so repeated calls do not re-map GBs of memory.
+        int dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64 && !g_pool_ready[dev].exchange(true)) {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t thr = UINT64_MAX;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+        }
         void* p = nullptr;
         const cudaError_t e = cudaMallocAsync(&p, need, c.stream);
         if (e != cudaSuccess) {
@@ -774,11 +787,16 @@ knng_status knng_merge(const void* vecA, int64_t nA, const uint32_t* idsA, const
     const size_t vbytes = static_cast<size_t>(n) * d * esz;
     char* ws = nullptr;
     if ((s = get_workspace(c, workspace, workspace_bytes, R.L.total + align_up(vbytes), &ws))) return s;
-    // combined vector set [S1; S2] (S = S1 U S2)
-    char* X = ws + R.L.total;
-    cudaMemcpyAsync(X, vecA, static_cast<size_t>(nA) * d * esz, cudaMemcpyDeviceToDevice, c.stream);
-    cudaMemcpyAsync(X + static_cast<size_t>(nA) * d * esz, vecB, static_cast<size_t>(nB) * d * esz,
-                    cudaMemcpyDeviceToDevice, c.stream);
+    // combined vector set [S1; S2] (S = S1 U S2); used in place when
+    // the caller's B rows already follow A's (the sharded tree's layout)
+    const char* X = static_cast<const char*>(vecA);
+    if (static_cast<const char*>(vecB) != X + static_cast<size_t>(nA) * d * esz) {
+        char* Xc = ws + R.L.total;
+        cudaMemcpyAsync(Xc, vecA, static_cast<size_t>(nA) * d * esz, cudaMemcpyDeviceToDevice, c.stream);
+        cudaMemcpyAsync(Xc + static_cast<size_t>(nA) * d * esz, vecB, static_cast<size_t>(nB) * d * esz,
+                        cudaMemcpyDeviceToDevice, c.stream);
+        X = Xc;
+    }
     R.D = Dims{n, d, k, sample_size, 2 * sample_size};
     R.X = X;
     R.dt = dt;
