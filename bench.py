@@ -41,7 +41,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--rows", dest="n", type=int, default=1_000_000,
+                    help="rows per GPU (C2: 10^6)")
     ap.add_argument("--k", type=int, default=32)
     ap.add_argument("--p", type=int, default=16)
     ap.add_argument("--iters", type=int, default=7)
@@ -50,6 +51,9 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=20_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--merge-iters", type=int, default=6,
+                    help="GGM refine iterations per tree level (N>1, and the N=1 GGM line)")
+    ap.add_argument("--no-ggm", action="store_true", help="skip the N=1 GGM measurement")
     return ap.parse_args()
 
 
@@ -116,10 +120,14 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def workload(args, rank):
+def workload(args, rank, world=1):
+    """N=1: the C2 SIFT1M-shaped set.  N>1: shard `rank` of an N x 1M
+    SIFT-shaped set (one mixture with 1000 N components, rows from the
+    stream (1, rank)) -- the sharded build's weak-scaling workload."""
     import datagen
-    X = datagen.make("sift", args.n, seed=1 + rank)
-    return X
+    if world == 1:
+        return datagen.make("sift", args.n, seed=1)
+    return datagen.make("sift", args.n, seed=1, part=rank, components=1000 * world)
 
 
 def cpu_baseline(args, X) -> dict:
@@ -164,6 +172,61 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def recall_at_10(K, Xd, dists, nodes):
+    """recall@10 on `nodes` sampled nodes against the exact k-NN
+    (knng_bruteforce), with the D27 tie rule: entry j of the first 10 counts
+    iff d(i, j) <= d_true,10(i)."""
+    import torch
+
+    import datagen
+    q = datagen.sample_nodes(Xd.shape[0], nodes)
+    _, gd = K.knng_bruteforce(Xd, torch.from_numpy(q), 10)
+    mine = dists[torch.from_numpy(q).cuda().long(), :10]
+    return float((mine <= gd[:, 9:10]).float().mean().item()), len(q)
+
+
+def measure_ggm(args, K, Xd, stream):
+    """GGM (Alg. 3) on the bench workload split in two halves:
+    knng_build per half, then knng_merge timed with CUDA events on the
+    launch stream."""
+    import torch
+    n, d = Xd.shape
+    h = n // 2
+    XA, XB = Xd[:h], Xd[h:]  # contiguous: knng_merge uses them in place
+    ia, da = K.knng_build(XA, args.k, args.iters, args.p, args.seed, stream=stream)
+    ib, db = K.knng_build(XB, args.k, args.iters, args.p, args.seed + 1, stream=stream)
+    ws = torch.empty(K.lib().knng_merge_workspace_bytes(K.KNNG_F32, h, n - h, d, args.k, args.p, 0),
+                     dtype=torch.uint8, device="cuda")
+
+    def merge():
+        return K.knng_merge(XA, ia, da, XB, ib, db, args.k, args.merge_iters, args.p, seed=args.seed, level=0,
+                            workspace=ws, stream=stream)
+
+    for _ in range(2):
+        merge()
+    torch.cuda.synchronize()
+    K.knng_set_timing(True)
+    K.knng_reset_timing()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = max(1, args.steps)
+    e0.record(stream)
+    for _ in range(reps):
+        mi, md = merge()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    K.knng_set_timing(False)
+    ms = e0.elapsed_time(e1) / reps
+    join_ms, join_launches = K.knng_kernel_time("k_join")
+    st = K.knng_last_stats()
+    rec, nq = recall_at_10(K, Xd, md, args.recall_nodes)
+    return {"workload": f"C2 split into 2 x {h} (knng_build per half, seeds {args.seed}/{args.seed + 1}), "
+                        f"then knng_merge", "merge_iters": args.merge_iters, "ms_per_merge": ms,
+            "recall_at_10": rec, "recall_nodes": nq,
+            "join_ms_per_launch": join_ms / max(1, join_launches),
+            "dist_evals": sum(s["dist_evals"] for s in st), "accepted": sum(s["accepted"] for s in st),
+            "dist_evals_per_s": sum(s["dist_evals"] for s in st) / (ms * 1e-3)}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -173,19 +236,41 @@ def main():
     import torch.distributed as dist
 
     import paper_2103_15386_b200.knng as K
+    from paper_2103_15386_b200.sharded import CudaOps, knng_build_sharded
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # KNNG_BENCH_BACKEND=gloo (testing only): several ranks sharing one GPU;
+    # the product exchange is NCCL.
+    backend = os.environ.get("KNNG_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    coll_dev = "cuda" if backend == "nccl" else "cpu"
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    X = workload(args, rank)
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], device=coll_dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def gather_rows(t):
+        """all ranks' row blocks concatenated (for the recall check only)."""
+        parts = [torch.empty_like(t, device=coll_dev) for _ in range(world)]
+        dist.all_gather(parts, t.to(coll_dev))
+        return torch.cat(parts).cuda()
+
+    X = workload(args, rank, world)
     n, d = X.shape
     Xd = torch.from_numpy(X).cuda()
     stream = torch.cuda.current_stream()
@@ -194,8 +279,30 @@ def main():
     ids = torch.empty((n, args.k), dtype=torch.int32, device="cuda")
     dists = torch.empty((n, args.k), dtype=torch.float32, device="cuda")
 
+    class Ops(CudaOps):
+        """The product compute, recording each call's iteration counters."""
+        history: list = []
+
+        def build(self, *a):
+            r = super().build(*a)
+            self.history.extend(K.knng_last_stats())
+            return r
+
+        def merge(self, *a):
+            r = super().merge(*a)
+            self.history.extend(K.knng_last_stats())
+            return r
+
+    ops = Ops(stream=stream)
+    out = {}
+
     def step():
-        K.knng_build(Xd, args.k, args.iters, args.p, args.seed, "l2", ids, dists, ws, stream)
+        if world == 1:
+            K.knng_build(Xd, args.k, args.iters, args.p, args.seed, "l2", ids, dists, ws, stream)
+            ops.history.extend(K.knng_last_stats())
+        else:  # one shard per GPU, log-depth GGM tree over NCCL (sharded.py)
+            out["g"] = knng_build_sharded(Xd, world, args.k, args.iters, args.merge_iters, args.p, args.seed,
+                                          ops=ops)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -204,6 +311,7 @@ def main():
     # ---- timed region: device time with CUDA events on the launch stream
     K.knng_set_timing(True)
     K.knng_reset_timing()
+    ops.history.clear()
     clocks = ClockSampler(local)
     clocks.start()
     launches0 = K.knng_launch_count()
@@ -219,23 +327,23 @@ def main():
     launches = K.knng_launch_count() - launches0
     clk = clocks.stop()
     K.knng_set_timing(False)
-    ms = e0.elapsed_time(e1) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     join_ms, join_launches = K.knng_kernel_time("k_join")
+    history = list(ops.history)
     stats = K.knng_last_stats()
+    exact_u8 = bool(K.knng_get_option("last_exact_u8"))
 
     # ---- quality: recall@10 on sampled nodes vs exact brute force (GPU)
-    import datagen
-    q = datagen.sample_nodes(n, args.recall_nodes)
-    gi, gd = K.knng_bruteforce(Xd, torch.from_numpy(q), 10)
-    g_thr = gd[:, 9:10]
-    mine = dists[torch.from_numpy(q).cuda().long(), :10]
-    recall = float((mine <= g_thr).float().mean().item())
+    if world > 1:
+        my_i, my_d = out["g"]
+        Xall = gather_rows(Xd)
+        Dall = gather_rows(my_d.contiguous())
+        recall, nq = recall_at_10(K, Xall, Dall, args.recall_nodes) if rank == 0 else (None, 0)
+        del Xall, Dall
+    else:
+        recall, nq = recall_at_10(K, Xd, dists, args.recall_nodes)
 
-    # ---- end to end through the public host API (pinned buffers, copies timed)
+    # ---- end to end through the public API (pinned host buffers, copies timed)
     e2e = None
     if not args.no_e2e:
         Xh = torch.from_numpy(X).pin_memory()
@@ -244,10 +352,18 @@ def main():
         lib = K.lib()
 
         def e2e_step():
-            st = lib.knng_build_host(Xh.data_ptr(), K.KNNG_F32, n, d, args.k, K.KNNG_L2SQ, args.iters, args.p,
-                                     args.seed, ih.data_ptr(), dh.data_ptr(), stream.cuda_stream)
-            if st != 0:
-                raise RuntimeError(K.knng_last_error())
+            if world == 1:
+                st = lib.knng_build_host(Xh.data_ptr(), K.KNNG_F32, n, d, args.k, K.KNNG_L2SQ, args.iters, args.p,
+                                         args.seed, ih.data_ptr(), dh.data_ptr(), stream.cuda_stream)
+                if st != 0:
+                    raise RuntimeError(K.knng_last_error())
+            else:
+                Xd.copy_(Xh, non_blocking=True)
+                gi, gd = knng_build_sharded(Xd, world, args.k, args.iters, args.merge_iters, args.p, args.seed,
+                                            ops=CudaOps(stream=stream))
+                ih.copy_(gi, non_blocking=True)
+                dh.copy_(gd, non_blocking=True)
+                torch.cuda.synchronize()
 
         e2e_step()
         barrier()
@@ -256,30 +372,28 @@ def main():
         for _ in range(args.steps):
             e2e_step()
         torch.cuda.synchronize()
-        e2e_s = (time.perf_counter() - t0) / args.steps
-        if world > 1:
-            t = torch.tensor([e2e_s], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_s = float(t.item())
+        e2e_s = max_over_ranks((time.perf_counter() - t0) / args.steps)
+        barrier()
         e2e = {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(X.nbytes),
-               "d2h_bytes_per_step": int(n * args.k * 8)}
+               "d2h_bytes_per_step": int(n * args.k * 8),
+               "api": "knng_build_host" if world == 1 else "knng_build_sharded (per-rank H2D/D2H)"}
 
     # ---- roofline of the dominant kernel (k_join), DESIGN.md section 6:
     # HBM view: algorithmic gather bytes = rows x (d x element + 4 id bytes);
     # ALU view: the canonical tile's minimum instruction count -- f32: FADD +
     # FFMA per dim and pair; exact-u8: VABSDIFF4 + IDP4A per 4 dims and pair
     # -- against the SM issue peak (148 SMs x 4 warp-instr/cycle x clock).
-    exact_u8 = bool(K.knng_get_option("last_exact_u8"))
     esz = 1 if exact_u8 else 4
-    nst = max(1, len(stats))
-    rows = sum(s["rows"] for s in stats)
-    evals = sum(s["dist_evals"] for s in stats)
-    alg_bytes_per_launch = rows * (d * esz + 4) / nst
-    join_avg_ms = join_ms / max(1, join_launches)
+    rows = sum(s["rows"] for s in history)
+    evals = sum(s["dist_evals"] for s in history)
+    accepted = sum(s["accepted"] for s in history)
+    launches_in_hist = max(1, join_launches)
+    alg_bytes_per_launch = rows * (d * esz + 4) / launches_in_hist
+    join_avg_ms = join_ms / launches_in_hist
     achieved_gbs = alg_bytes_per_launch / (join_avg_ms * 1e-3) / 1e9 if join_avg_ms > 0 else 0.0
     peak, peak_kind = peaks()
     instr_per_dim_pair = 0.5 if exact_u8 else 2.0
-    warp_instr = evals * d * instr_per_dim_pair / 32 / nst
+    warp_instr = evals * d * instr_per_dim_pair / 32 / launches_in_hist
     clk_ghz = (clk.get("sm_mhz") or 1965.0) / 1000.0
     issue_peak = 148 * 4 * clk_ghz * 1e9
     issue_rate = warp_instr / (join_avg_ms * 1e-3) if join_avg_ms > 0 else 0.0
@@ -290,17 +404,21 @@ def main():
         traffic = tj.get("u8" if exact_u8 else "f32")
     except Exception:
         pass
-    hbm_frac = achieved_gbs / peak
-    alu_frac = issue_rate / issue_peak
     alu = {"bound": "alu", "achieved": issue_rate / 1e9, "peak": issue_peak / 1e9,
-           "unit": "G warp-instr/s", "frac": alu_frac,
+           "unit": "G warp-instr/s", "frac": issue_rate / issue_peak,
            "instr_per_dim_pair": instr_per_dim_pair, "sm_clock_ghz": clk_ghz}
     roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
-                "frac": hbm_frac, "traffic": traffic, "peak_source": peak_kind,
+                "frac": achieved_gbs / peak, "traffic": traffic, "peak_source": peak_kind,
                 "kernel": "k_join", "avg_launch_ms": join_avg_ms, "launches": join_launches,
                 "share_of_step": join_ms / args.steps / ms if ms > 0 else None,
                 "alg_bytes_per_launch": alg_bytes_per_launch, "element_bytes": esz,
                 "alu": alu}
+    throughput = {"dist_evals_per_s": evals / args.steps / (ms * 1e-3),
+                  "accepted_updates_per_s": accepted / args.steps / (ms * 1e-3), "per": "rank 0"}
+
+    ggm = None
+    if world == 1 and not args.no_ggm:
+        ggm = measure_ggm(args, K, Xd, stream)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -308,19 +426,25 @@ def main():
         cpu.pop("sample_seconds", None)
 
     if rank == 0:
+        if world == 1:
+            cfg = {"workload": "C2 SIFT1M-shaped (BASELINE.json configs[1])", "n": n, "d": d, "k": args.k,
+                   "sample_size": args.p, "iters": args.iters, "metric": "l2",
+                   "l2_flush": "inputs (512 MB) larger than L2"}
+        else:
+            cfg = {"workload": f"sharded SIFT-shaped {world} x {n} (one 1M shard per GPU, log-depth GGM tree "
+                               f"over NCCL; C4/C5 scheme at C2 shard size)", "n": world * n, "n_per_gpu": n,
+                   "d": d, "k": args.k, "sample_size": args.p, "iters": args.iters,
+                   "merge_iters": args.merge_iters, "shards": world, "metric": "l2",
+                   "l2_flush": "inputs (512 MB per GPU) larger than L2"}
         line = {"metric": METRIC, "value": ms / 1000.0, "unit": "s", "n_gpus": world, "steps": args.steps,
                 "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
                 "vs_baseline": None, "dtype": "u8" if exact_u8 else "f32",
-                "data": "synthetic GMM-LR SIFT-shaped (datagen 'sift', seed 1+rank), integer-valued fp32 input"
+                "data": "synthetic GMM-LR SIFT-shaped (datagen 'sift'), integer-valued fp32 input"
                         + ("; built on the exact uint8 path (option exact_u8: graph bit-identical to fp32)"
                            if exact_u8 else ""),
-                "config": {"workload": "C2 SIFT1M-shaped (BASELINE.json configs[1])", "n": n, "d": d,
-                           "k": args.k, "sample_size": args.p, "iters": args.iters, "metric": "l2",
-                           "l2_flush": "inputs (512 MB) larger than L2", "per_rank": "one 1M build per GPU"},
-                "recall_at_10": recall, "recall_nodes": len(q),
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-                "clocks": clk,
-                "iter_stats": stats}
+                "config": cfg, "recall_at_10": recall, "recall_nodes": nq,
+                "roofline": roofline, "throughput": throughput, "ggm": ggm, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(launches), "clocks": clk, "iter_stats": stats}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

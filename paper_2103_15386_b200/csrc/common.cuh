@@ -61,30 +61,43 @@ __device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
     return __shfl_xor_sync(kFull, v, m);
 }
 
-// Bitonic sort of one u64 per lane, ascending across lanes 0..31.  Each
-// compare-exchange is one comparison and one select (branch-free).
+// Bitonic sorting networks, one value per lane, ascending across lanes.
+// Direction by complement: during phase k2 the lanes of a descending block
+// hold ~x (bitwise NOT reverses the unsigned order), so every compare-
+// exchange of the phase is ascending and the lower lane of a pair keeps the
+// minimum: x <- ((o < x) != upper) ? o : x  (taking an equal o is a no-op).
+// One u64 compare + two selects per stage (the complement costs two LOPs
+// per phase), instead of a per-stage direction test.
 __device__ __forceinline__ uint64_t warp_sort_u64(uint64_t x) {
     const uint32_t lane = lane_id();
+    uint32_t m_prev = 0;
 #pragma unroll
     for (int k2 = 2; k2 <= 32; k2 <<= 1) {
+        const uint32_t m = (k2 < 32 && (lane & k2)) ? 0xFFFFFFFFu : 0u;
+        const uint32_t t = m ^ m_prev;
+        x ^= (static_cast<uint64_t>(t) << 32) | t;
+        m_prev = m;
 #pragma unroll
         for (int j = k2 >> 1; j > 0; j >>= 1) {
             const uint64_t o = shfl_xor_u64(x, j);
-            const bool keep_min = ((lane & j) == 0) == ((lane & k2) == 0);
-            x = (keep_min ? (o < x) : (x < o)) ? o : x;
+            const bool upper = (lane & j) != 0;
+            x = ((o < x) != upper) ? o : x;
         }
     }
     return x;
 }
 __device__ __forceinline__ uint32_t warp_sort_u32(uint32_t x) {
     const uint32_t lane = lane_id();
+    uint32_t m_prev = 0;
 #pragma unroll
     for (int k2 = 2; k2 <= 32; k2 <<= 1) {
+        const uint32_t m = (k2 < 32 && (lane & k2)) ? 0xFFFFFFFFu : 0u;
+        x ^= m ^ m_prev;
+        m_prev = m;
 #pragma unroll
         for (int j = k2 >> 1; j > 0; j >>= 1) {
             const uint32_t o = __shfl_xor_sync(kFull, x, j);
-            const bool keep_min = ((lane & j) == 0) == ((lane & k2) == 0);
-            x = keep_min ? min(o, x) : max(o, x);
+            x = (lane & j) ? max(o, x) : min(o, x);
         }
     }
     return x;
@@ -95,7 +108,8 @@ __device__ __forceinline__ uint64_t warp_bitonic_merge_u64(uint64_t x) {
 #pragma unroll
     for (int j = 16; j > 0; j >>= 1) {
         const uint64_t o = shfl_xor_u64(x, j);
-        x = (((lane & j) == 0) ? (o < x) : (x < o)) ? o : x;
+        const bool upper = (lane & j) != 0;
+        x = ((o < x) != upper) ? o : x;
     }
     return x;
 }
@@ -108,7 +122,9 @@ __device__ __forceinline__ uint64_t warp_bitonic_merge_u64(uint64_t x) {
 // newcomers get NEW | from-bucket.  Keys are compared as (key << 1) | origin
 // (origin 0 = list, 1 = candidate): dist >= 0 leaves bit 63 free, so the
 // shifted order is (dist, id, origin), and duplicates keep the list entry.
-__device__ __forceinline__ void warp_merge_list(uint64_t& L, uint32_t& bits, uint64_t cand) {
+// scratch: 32 u64 of per-warp shared memory (compaction by scatter: each
+// surviving element writes its rank's slot).
+__device__ __forceinline__ void warp_merge_list(uint64_t& L, uint32_t& bits, uint64_t cand, uint64_t* scratch) {
     const uint32_t lane = lane_id();
     uint64_t x = cand == kSentinel ? kSentinel : ((cand << 1) | 1ull);
     x = warp_sort_u64(x);
@@ -127,15 +143,16 @@ __device__ __forceinline__ void warp_merge_list(uint64_t& L, uint32_t& bits, uin
     const bool hi_ok = hi != kSentinel && (hi >> 1) != (hi_prev >> 1);
     const uint32_t lo_m = __ballot_sync(kFull, lo_ok), hi_m = __ballot_sync(kFull, hi_ok);
     const int nlo = __popc(lo_m);
-    // compaction: output lane j takes the j-th surviving element
-    const int j = static_cast<int>(lane);
-    const int src_lo = j < nlo ? static_cast<int>(__fns(lo_m, 0, j + 1)) : 0;
-    const int jh = j - nlo;
-    const int src_hi = (jh >= 0 && jh < __popc(hi_m)) ? static_cast<int>(__fns(hi_m, 0, jh + 1)) : 0;
-    const uint64_t from_lo = shfl_u64(lo, src_lo), from_hi = shfl_u64(hi, src_hi);
-    uint64_t e = kSentinel;
-    if (j < nlo) e = from_lo;
-    else if (jh < __popc(hi_m)) e = from_hi;
+    // compaction: the j-th surviving element goes to slot j (< 32 kept)
+    const int r_lo = __popc(lo_m & lanemask_lt());
+    const int r_hi = nlo + __popc(hi_m & lanemask_lt());
+    __syncwarp();
+    scratch[lane] = kSentinel;
+    __syncwarp();
+    if (lo_ok) scratch[r_lo] = lo;
+    if (hi_ok && r_hi < 32) scratch[r_hi] = hi;
+    __syncwarp();
+    const uint64_t e = scratch[lane];
     // bits: a list-origin element is the r-th list element kept, r = number
     // of list-origin elements before it (the merge preserves their order)
     const bool is_list = e != kSentinel && !(e & 1ull);

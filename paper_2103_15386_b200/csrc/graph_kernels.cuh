@@ -116,10 +116,11 @@ __global__ void k_merge_sample(Dims D, Graph G, Samples S, int do_merge, int do_
     if (do_merge) {
         const uint32_t c = G.bcnt[s];
         if (c > 0) {
+            extern __shared__ uint64_t ms_scratch[];  // 32 u64 per warp
             const uint64_t* bk = G.bucket + G.boff[s];
             for (uint32_t base = 0; base < c; base += 32) {
                 const uint64_t cand = (base + lane < c) ? bk[base + lane] : kSentinel;
-                warp_merge_list(cur.key, cur.meta, cand);
+                warp_merge_list(cur.key, cur.meta, cand, ms_scratch + (threadIdx.x >> 5) * 32);
             }
             changed = true;
             if (!in_list) cur = Elem{kSentinel, 0u};
@@ -251,16 +252,20 @@ __global__ void k_rev_scatter(Dims D, Samples S) {
 
 // sort + dedup one u32 id per lane (0xFFFFFFFF = empty, sorts last); returns
 // the unique sorted ids compacted to lanes [0, count) and sets count.
-__device__ __forceinline__ uint32_t warp_sort_unique_ids(uint32_t id, int& count) {
+// scratch: 32 u32 of per-warp shared memory (compaction by rank scatter).
+__device__ __forceinline__ uint32_t warp_sort_unique_ids(uint32_t id, int& count, uint32_t* scratch) {
     const uint32_t lane = lane_id();
     const uint32_t x = warp_sort_u32(id);
     const uint32_t prev = __shfl_sync(kFull, x, (lane + 31) & 31);
     const bool ok = x != 0xFFFFFFFFu && (lane == 0 || x != prev);
     const uint32_t okm = __ballot_sync(kFull, ok);
     count = __popc(okm);
-    const int src = static_cast<int>(lane) < count ? static_cast<int>(__fns(okm, 0, lane + 1)) : 0;
-    const uint32_t got = __shfl_sync(kFull, x, src);
-    return static_cast<int>(lane) < count ? got : 0xFFFFFFFFu;
+    __syncwarp();
+    scratch[lane] = 0xFFFFFFFFu;
+    __syncwarp();
+    if (ok) scratch[__popc(okm & lanemask_lt())] = x;
+    __syncwarp();
+    return scratch[lane];
 }
 
 // One warp per node v: G(v) = sort_unique(F(v) U c smallest-priority reverse
@@ -273,6 +278,8 @@ __global__ void k_rev_select(Dims D, Samples S, uint32_t tword, uint64_t seed) {
     const uint32_t lane = lane_id();
     const uint2 key = seed_key(seed);
     const int p = D.p, cap = D.cap;
+    extern __shared__ uint32_t rs_scratch[];  // 64 u32 per warp
+    uint32_t* scr = rs_scratch + (threadIdx.x >> 5) * 64;
     uint32_t gnew = 0xFFFFFFFFu;
     int m = 0;
     for (int f = 0; f < 2; ++f) {
@@ -306,19 +313,29 @@ __global__ void k_rev_select(Dims D, Samples S, uint32_t tword, uint64_t seed) {
             if (j >= 0 && j < c) e = static_cast<uint32_t>(got);
         }
         int cnt = 0;
-        uint32_t u = warp_sort_unique_ids(e, cnt);
+        uint32_t u = warp_sort_unique_ids(e, cnt, scr);
         if (f == 0) {
             gnew = u;
             m = cnt;
         } else {
-            // D11: drop ids that are also NEW samples
-            bool in_new = false;
-            for (int t = 0; t < m; ++t) in_new |= (__shfl_sync(kFull, gnew, t) == u);
+            // D11: drop ids that are also NEW samples (binary search in the
+            // sorted G_new held in shared memory)
+            scr[32 + lane] = gnew;
+            __syncwarp();
+            int lo = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1)
+                if (lo + step <= m && scr[32 + lo + step - 1] < u) lo += step;
+            const bool in_new = lo < m && scr[32 + lo] == u;
             const bool keep = static_cast<int>(lane) < cnt && !in_new;
             const uint32_t km = __ballot_sync(kFull, keep);
             cnt = __popc(km);
-            const int src = static_cast<int>(lane) < cnt ? static_cast<int>(__fns(km, 0, lane + 1)) : 0;
-            u = __shfl_sync(kFull, u, src);
+            __syncwarp();
+            scr[lane] = 0xFFFFFFFFu;
+            __syncwarp();
+            if (keep) scr[__popc(km & lanemask_lt())] = u;
+            __syncwarp();
+            u = scr[lane];
         }
         if (static_cast<int>(lane) < cnt) S.G[static_cast<size_t>(f) * D.n * cap + static_cast<size_t>(v) * cap + lane] = u;
         if (lane == 0) {

@@ -302,7 +302,7 @@ struct Run {
         const int grid = warps_grid(D.n, wpb);
         DevStats* ps = prev_iter >= 0 ? stats + prev_iter : nullptr;
         c.launch(do_sample ? "k_merge_sample" : "k_merge", [&] {
-            k_merge_sample<<<grid, wpb * 32, wpb * 32 * sizeof(Elem), c.stream>>>(D, G, S, do_merge, do_sample, ps);
+            k_merge_sample<<<grid, wpb * 32, wpb * 32 * sizeof(uint64_t), c.stream>>>(D, G, S, do_merge, do_sample, ps);
         });
     }
 
@@ -321,7 +321,7 @@ struct Run {
         });
         const int wpb = 8;
         c.launch("k_rev_select", [&] {
-            k_rev_select<<<warps_grid(D.n, wpb), wpb * 32, 0, c.stream>>>(D, S, tword, seed);
+            k_rev_select<<<warps_grid(D.n, wpb), wpb * 32, wpb * 64 * sizeof(uint32_t), c.stream>>>(D, S, tword, seed);
         });
     }
 
