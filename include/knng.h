@@ -66,6 +66,9 @@ typedef struct {
                              into its bucket)                                */
     int64_t accepted;     /* list entries that are new after the update      */
     int64_t rows;         /* vector rows gathered by the join kernel          */
+    int64_t recomputed;   /* canonical distance recomputations of the float
+                             tensor-core join (its exact-selection window);
+                             0 for the other join kernels                    */
 } knng_iter_stats;
 
 /* ------------------------------------------------------------------------
@@ -186,7 +189,12 @@ knng_status knng_debug_philox(const uint32_t* ctr, int64_t m, uint64_t seed,
  *                  1: the batched cp.async join (join_kernel.cuh);
  *                  2: always the warp-specialised join;
  *                  3: the lock-step ALU join (join_ls.cuh) where the
- *                     tensor-core join would run.
+ *                     tensor-core join would run;
+ *                  4: float rows (L2 / cosine, d % 4 == 0, d <= 128): the
+ *                     TF32 tensor-core join (join_tcf.cuh) -- exact
+ *                     selection by canonical recomputation inside an
+ *                     a-priori error window; slower than the CUDA-core
+ *                     join on B200, so opt-in.
  *                  All produce bit-identical graphs.
  *   "last_exact_u8" (read-only) 1 if the last build/merge on this thread ran
  *                  on the exact integer path.

@@ -86,6 +86,28 @@ __device__ __forceinline__ uint64_t warp_sort_u64(uint64_t x) {
     }
     return x;
 }
+// Bitonic sort of every block of P lanes (P = 2, 4, ..., 32), ascending.
+// When only the first P lanes hold data and the rest kSentinel, the whole
+// warp is ascending after log2(P) phases instead of 5.
+__device__ __forceinline__ uint64_t warp_sort_u64_blocks(uint64_t x, int P) {
+    const uint32_t lane = lane_id();
+    uint32_t m_prev = 0;
+#pragma unroll
+    for (int k2 = 2; k2 <= 32; k2 <<= 1) {
+        if (k2 > P) break;
+        const uint32_t m = (k2 < P && (lane & k2)) ? 0xFFFFFFFFu : 0u;
+        const uint32_t t = m ^ m_prev;
+        x ^= (static_cast<uint64_t>(t) << 32) | t;
+        m_prev = m;
+#pragma unroll
+        for (int j = k2 >> 1; j > 0; j >>= 1) {
+            const uint64_t o = shfl_xor_u64(x, j);
+            const bool upper = (lane & j) != 0;
+            x = ((o < x) != upper) ? o : x;
+        }
+    }
+    return x;
+}
 __device__ __forceinline__ uint32_t warp_sort_u32(uint32_t x) {
     const uint32_t lane = lane_id();
     uint32_t m_prev = 0;
@@ -124,10 +146,12 @@ __device__ __forceinline__ uint64_t warp_bitonic_merge_u64(uint64_t x) {
 // shifted order is (dist, id, origin), and duplicates keep the list entry.
 // scratch: 32 u64 of per-warp shared memory (compaction by scatter: each
 // surviving element writes its rank's slot).
-__device__ __forceinline__ void warp_merge_list(uint64_t& L, uint32_t& bits, uint64_t cand, uint64_t* scratch) {
+// P: candidates occupy lanes [0, P) only (the rest kSentinel), P a power of 2.
+__device__ __forceinline__ void warp_merge_list(uint64_t& L, uint32_t& bits, uint64_t cand, uint64_t* scratch,
+                                                int P = 32) {
     const uint32_t lane = lane_id();
     uint64_t x = cand == kSentinel ? kSentinel : ((cand << 1) | 1ull);
-    x = warp_sort_u64(x);
+    x = warp_sort_u64_blocks(x, P);
     const uint64_t l = L == kSentinel ? kSentinel : (L << 1);
     const uint64_t xr = shfl_u64(x, 31 - lane);  // half-cleaner of l ++ reverse(x)
     uint64_t lo = xr < l ? xr : l;
@@ -155,6 +179,24 @@ __device__ __forceinline__ void warp_merge_list(uint64_t& L, uint32_t& bits, uin
     const uint64_t e = scratch[lane];
     // bits: a list-origin element is the r-th list element kept, r = number
     // of list-origin elements before it (the merge preserves their order)
+    const bool is_list = e != kSentinel && !(e & 1ull);
+    const int r = __popc(__ballot_sync(kFull, is_list) & lanemask_lt());
+    const uint32_t old_bits = __shfl_sync(kFull, bits, r);
+    bits = is_list ? old_bits : (e != kSentinel ? 3u : 0u);
+    L = e == kSentinel ? kSentinel : (e >> 1);
+}
+
+// List update when the candidates are already sorted, unique and disjoint
+// from the list (k_merge_sample's pre-filter): y holds (cand << 1) | 1 keys,
+// ascending, kSentinel tail.  The 32 smallest of the union are the lower
+// half of one half-cleaner -- one bitonic merge, no dedup.  Bits as in
+// warp_merge_list.
+__device__ __forceinline__ void warp_merge_list_disjoint(uint64_t& L, uint32_t& bits, uint64_t y) {
+    const uint32_t lane = lane_id();
+    const uint64_t l = L == kSentinel ? kSentinel : (L << 1);
+    const uint64_t yr = shfl_u64(y, 31 - lane);
+    uint64_t e = yr < l ? yr : l;
+    e = warp_bitonic_merge_u64(e);
     const bool is_list = e != kSentinel && !(e & 1ull);
     const int r = __popc(__ballot_sync(kFull, is_list) & lanemask_lt());
     const uint32_t old_bits = __shfl_sync(kFull, bits, r);

@@ -8,7 +8,7 @@
 namespace knng {
 
 struct DevStats {  // device mirror of knng_iter_stats
-    unsigned long long joins, sum_m, sum_q, dist_evals, candidates, appended, accepted, rows;
+    unsigned long long joins, sum_m, sum_q, dist_evals, candidates, appended, accepted, rows, recomputed;
 };
 
 // Bucketed bulk update (D17): the candidates of one iteration for target t
@@ -28,7 +28,7 @@ struct Samples {
     uint32_t* fwd;   // [2][n][p]   forward NEW / OLD samples
     uint8_t* fcnt;   // [n][2]
     uint32_t* rcnt;  // [2][n]      reverse counts
-    uint32_t* rcur;  // [2][n]      reverse scatter cursors
+    uint32_t* fpos;  // [2][n][p]   slot of forward sample (s, j) in its target's reverse list
     uint64_t* off;   // [3][n+1]    CSR offsets: reverse NEW, reverse OLD, buckets
     uint32_t* rsrc;  // [2][n*p]    reverse sources
     uint32_t* G;     // [2][n][cap] G_new / G_old, sorted unique
@@ -116,11 +116,49 @@ __global__ void k_merge_sample(Dims D, Graph G, Samples S, int do_merge, int do_
     if (do_merge) {
         const uint32_t c = G.bcnt[s];
         if (c > 0) {
-            extern __shared__ uint64_t ms_scratch[];  // 32 u64 per warp
+            extern __shared__ uint64_t ms_scratch[];  // 64 u64 per warp: scratch, list copy
+            uint64_t* scr = ms_scratch + (threadIdx.x >> 5) * 64;
+            uint64_t* lst = scr + 32;
             const uint64_t* bk = G.bucket + G.boff[s];
             for (uint32_t base = 0; base < c; base += 32) {
                 const uint64_t cand = (base + lane < c) ? bk[base + lane] : kSentinel;
-                warp_merge_list(cur.key, cur.meta, cand, ms_scratch + (threadIdx.x >> 5) * 32);
+                // Pre-filter (exact): a candidate equal to a list key is the
+                // same id (D5 keys are canonical per id) and one not below the
+                // current k-th key cannot enter the k smallest.  Only the
+                // survivors go through the sorting network.
+                const uint64_t kth = shfl_u64(cur.key, k - 1);
+                __syncwarp();
+                lst[lane] = cur.key;
+                __syncwarp();
+                int pos = 0;
+#pragma unroll
+                for (int step = 16; step > 0; step >>= 1)
+                    if (lst[pos + step - 1] < cand) pos += step;
+                const bool keep = cand < kth && lst[pos] != cand;
+                const uint32_t km = __ballot_sync(kFull, keep);
+                if (km == 0) continue;
+                const int cnt = __popc(km);
+                __syncwarp();
+                scr[lane] = kSentinel;
+                __syncwarp();
+                if (keep) scr[__popc(km & lanemask_lt())] = (cand << 1) | 1ull;
+                __syncwarp();
+                // sort the survivors (network sized to their count), drop
+                // repeated candidates, merge with the list
+                const int P = cnt <= 2 ? 2 : cnt <= 4 ? 4 : cnt <= 8 ? 8 : cnt <= 16 ? 16 : 32;
+                uint64_t y = warp_sort_u64_blocks(scr[lane], P);
+                const uint64_t prev = shfl_u64(y, (lane + 31) & 31);
+                const bool uniq = y != kSentinel && (lane == 0 || y != prev);
+                const uint32_t um = __ballot_sync(kFull, uniq);
+                if (__popc(um) != cnt) {  // repeats present: re-compact
+                    __syncwarp();
+                    scr[lane] = kSentinel;
+                    __syncwarp();
+                    if (uniq) scr[__popc(um & lanemask_lt())] = y;
+                    __syncwarp();
+                    y = scr[lane];
+                }
+                warp_merge_list_disjoint(cur.key, cur.meta, y);
             }
             changed = true;
             if (!in_list) cur = Elem{kSentinel, 0u};
@@ -141,12 +179,13 @@ __global__ void k_merge_sample(Dims D, Graph G, Samples S, int do_merge, int do_
         const uint32_t id = key_id(cur.key);
         if (isnew && rn < p) {
             S.fwd[static_cast<size_t>(s) * p + rn] = id;
-            atomicAdd(S.rcnt + id, 1u);
+            // the count's old value is this sample's slot in the reverse CSR
+            S.fpos[static_cast<size_t>(s) * p + rn] = atomicAdd(S.rcnt + id, 1u);
             cur.meta &= ~1u;  // "Mark all sampled neighbors as OLD"
         }
         if (isold && ro < p) {
             S.fwd[static_cast<size_t>(D.n) * p + static_cast<size_t>(s) * p + ro] = id;
-            atomicAdd(S.rcnt + D.n + id, 1u);
+            S.fpos[static_cast<size_t>(D.n) * p + static_cast<size_t>(s) * p + ro] = atomicAdd(S.rcnt + D.n + id, 1u);
         }
         if (lane == 0) {
             S.fcnt[2 * s] = static_cast<uint8_t>(min(__popc(newb), p));
@@ -236,8 +275,9 @@ __global__ void k_scan_final(Samples S, int64_t n, int64_t nblk) {
 }
 
 // reverse append of P:149 as a CSR scatter: s goes to the list of every v in
-// its forward samples.  Order inside a list is arbitrary; the selection that
-// follows is order-independent (D10).
+// its forward samples, at the slot its count atomic returned in
+// k_merge_sample (no second atomic).  Order inside a list is arbitrary; the
+// selection that follows is order-independent (D10).
 __global__ void k_rev_scatter(Dims D, Samples S) {
     const int f = blockIdx.y;
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -246,7 +286,7 @@ __global__ void k_rev_scatter(Dims D, Samples S) {
     const int j = static_cast<int>(i - s * D.p);
     if (j >= S.fcnt[2 * s + f]) return;
     const uint32_t v = S.fwd[static_cast<size_t>(f) * D.n * D.p + i];
-    const uint32_t pos = atomicAdd(S.rcur + f * D.n + v, 1u);
+    const uint32_t pos = S.fpos[static_cast<size_t>(f) * D.n * D.p + i];
     S.rsrc[static_cast<size_t>(f) * D.n * D.p + S.off[f * (D.n + 1) + v] + pos] = static_cast<uint32_t>(s);
 }
 
@@ -282,24 +322,41 @@ __global__ void k_rev_select(Dims D, Samples S, uint32_t tword, uint64_t seed) {
     uint32_t* scr = rs_scratch + (threadIdx.x >> 5) * 64;
     uint32_t gnew = 0xFFFFFFFFu;
     int m = 0;
+    // both flags' loads up front: counts, CSR bounds, forward row and the
+    // first 32 reverse sources (two dependent levels instead of six)
+    int fcv[2], rv[2];
+    uint64_t o0v[2];
+    uint32_t fw[2], pre[2];
+#pragma unroll
     for (int f = 0; f < 2; ++f) {
-        const int fc = S.fcnt[2 * v + f];
-        const uint32_t* fwd = S.fwd + static_cast<size_t>(f) * D.n * p + static_cast<size_t>(v) * p;
+        fcv[f] = S.fcnt[2 * v + f];
+        o0v[f] = S.off[f * (D.n + 1) + v];
+        rv[f] = static_cast<int>(S.off[f * (D.n + 1) + v + 1] - o0v[f]);
+        fw[f] = static_cast<int>(lane) < p ? S.fwd[static_cast<size_t>(f) * D.n * p + static_cast<size_t>(v) * p + lane]
+                                           : 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (int f = 0; f < 2; ++f)
+        pre[f] = static_cast<int>(lane) < rv[f] ? S.rsrc[static_cast<size_t>(f) * D.n * p + o0v[f] + lane] : 0xFFFFFFFFu;
+#pragma unroll
+    for (int f = 0; f < 2; ++f) {
+        const int fc = fcv[f];
         const uint32_t* rs = S.rsrc + static_cast<size_t>(f) * D.n * p;
-        const uint64_t o0 = S.off[f * (D.n + 1) + v], o1 = S.off[f * (D.n + 1) + v + 1];
-        const int r = static_cast<int>(o1 - o0);
+        const uint64_t o0 = o0v[f];
+        const int r = rv[f];
         const int c = cap - fc;
-        uint32_t e = 0xFFFFFFFFu;
-        if (static_cast<int>(lane) < fc) e = fwd[lane];
+        uint32_t e = static_cast<int>(lane) < fc ? fw[f] : 0xFFFFFFFFu;
         if (r <= c) {
+            // reverse source j sits in lane j of pre (r <= c <= 32)
             const int j = static_cast<int>(lane) - fc;
-            if (j >= 0 && j < r) e = rs[o0 + j];
+            const uint32_t got = __shfl_sync(kFull, pre[f], j >= 0 && j < r ? j : 0);
+            if (j >= 0 && j < r) e = got;
         } else {
             uint64_t best = kSentinel;  // running 32 smallest (prio, s), sorted
             for (int base = 0; base < r; base += 32) {
                 uint64_t x = kSentinel;
                 if (base + static_cast<int>(lane) < r) {
-                    const uint32_t src = rs[o0 + base + lane];
+                    const uint32_t src = base == 0 ? pre[f] : rs[o0 + base + lane];
                     const uint4 o = philox4x32_10(
                         make_uint4(f == 0 ? kTagRevNew : kTagRevOld, tword, src, static_cast<uint32_t>(v)), key);
                     x = (static_cast<uint64_t>(o.x) << 32) | src;
@@ -340,8 +397,7 @@ __global__ void k_rev_select(Dims D, Samples S, uint32_t tword, uint64_t seed) {
         if (static_cast<int>(lane) < cnt) S.G[static_cast<size_t>(f) * D.n * cap + static_cast<size_t>(v) * cap + lane] = u;
         if (lane == 0) {
             S.gcnt[2 * v + f] = static_cast<uint8_t>(cnt);
-            S.rcnt[f * D.n + v] = 0u;  // counts and cursors back to zero
-            S.rcur[f * D.n + v] = 0u;
+            S.rcnt[f * D.n + v] = 0u;  // counts back to zero for the next iteration
         }
     }
 }

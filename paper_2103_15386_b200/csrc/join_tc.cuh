@@ -35,7 +35,8 @@
 //     thread 0: kch MMAs (K = 32 each) of batch b -> TMEM, commit -> mbarrier
 //     wait MMA(b) -> rows[b & 1] is free: cp.async rows(b+2) into it (SW128
 //       K-major layout) and load their norms
-//     row scans of b (tcgen05.ld); filing of b / b-1 / b-2 (as join_ls)
+//     filing of b-1 / b-2 (as join_ls) while MMA(b) runs
+//     row scans of b (tcgen05.ld); keys of b and their targets' loads
 #pragma once
 #include <climits>
 
@@ -123,6 +124,23 @@ __device__ __forceinline__ uint32_t bit_range(int a, int b) {
     return hi & ~((1u << a) - 1u);
 }
 
+// L2 eviction-priority policies: the sample rows are re-read by many joins
+// (keep them: evict_last); sample lists and bucket appends stream through
+// (evict_first), so they do not push the rows out of L2.
+__device__ __forceinline__ uint64_t l2_policy_keep() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_stream() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void st_stream_u64(uint64_t* addr, uint64_t v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(addr), "l"(v), "l"(pol) : "memory");
+}
+
 __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
 k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Graph G, Samples S, int64_t boundary,
           unsigned long long* __restrict__ work, DevStats* __restrict__ stats) {
@@ -146,6 +164,7 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
     const int d = D.d, cap = D.cap;
     const bool restricted = boundary >= 0;
     const int kch = (d + 31) >> 5;  // MMAs of K = 32 (d % 16 == 0; zero-filled to 32)
+    const uint64_t pol_keep = l2_policy_keep(), pol_stream = l2_policy_stream();
 
     // ---------------------------------------------------------------- plans
     int cbuf = 1;
@@ -176,9 +195,11 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
                     const uint32_t* go = gn + static_cast<size_t>(D.n) * cap;
                     const uint32_t dn = smem_u32(cids + lane * 2 * cap), dq = dn + 4 * cap;
                     for (int c = 0; c < cap; c += 4) {
-                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dn + 4 * c), "l"(gn + c)
+                        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(dn + 4 * c),
+                                     "l"(gn + c), "l"(pol_stream)
                                      : "memory");
-                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dq + 4 * c), "l"(go + c)
+                        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(dq + 4 * c),
+                                     "l"(go + c), "l"(pol_stream)
                                      : "memory");
                     }
                 }
@@ -274,9 +295,9 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
             const uint8_t* src0 = X + part * 16;
             for (int slot = row0; slot < nslots; slot += 16) {
                 const uint32_t id = P.ids[slot];
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
+                asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(
                                  dbase + slot * 128 + ((part ^ (slot & 7)) << 4)),
-                             "l"(src0 + static_cast<size_t>(id) * d)
+                             "l"(src0 + static_cast<size_t>(id) * d), "l"(pol_keep)
                              : "memory");
             }
         } else if (part < kchunks) {
@@ -310,7 +331,7 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
     auto file_store = [&]() {
 #pragma unroll
         for (int r = 0; r < 2; ++r)
-            if (f2_key[r] != kSentinel) G.bucket[f2_pos[r]] = f2_key[r];
+            if (f2_key[r] != kSentinel) st_stream_u64(G.bucket + f2_pos[r], f2_key[r], pol_stream);
     };
     auto file_atomic = [&]() {
         const bool ok0 = f1_key[0] < f1_th, ok1 = f1_key[1] < f1_th;  // D17 (the sentinel never passes)
@@ -420,6 +441,9 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
             const int* nb = nrm + nbuf * kTcRows;
             const int ns = nb[s] >> 7;  // n_s
             int minA = INT_MAX, minB = INT_MAX;
+            // deferred filing of the two previous batches while MMA(b) runs
+            file_store();
+            file_atomic();
             mbar_wait(mma_bar, b & 1);
             tc_fence_after();
 
@@ -466,9 +490,7 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
             }
             tc_fence_before();
 
-            // ---- deferred filing of the two previous batches, then this one's keys
-            file_store();
-            file_atomic();
+            // ---- this batch's keys (filed in iterations b+1 and b+2)
             uint64_t k1 = kSentinel, k2 = kSentinel;
             if (act && minA != INT_MAX)
                 k1 = make_key(static_cast<float>(ns + (minA >> 7)), P.ids[minA & 127]);

@@ -17,6 +17,7 @@
 #include "join_kernel.cuh"
 #include "join_ls.cuh"
 #include "join_tc.cuh"
+#include "join_tcf.cuh"
 #include "join_ws.cuh"
 
 using namespace knng;
@@ -47,7 +48,7 @@ constexpr int kMaxIters = 256;
 
 // ---------------------------------------------------------------- layout
 struct Layout {
-    size_t keys, newmask, kth, bcnt, bucket, fwd, fcnt, rcnt, rcur, off, rsrc, G, gcnt, bsum, cand, stats,
+    size_t keys, newmask, kth, bcnt, bucket, fwd, fcnt, rcnt, fpos, off, rsrc, G, gcnt, bsum, cand, stats,
         xnorm, xu8, sqn, reserved, flag, total;
 };
 
@@ -73,7 +74,7 @@ Layout make_layout(int64_t n, int d, int k, int p, bool cosine, bool own_keys, b
     L.fwd = take(static_cast<size_t>(2) * n * p * 4);
     L.fcnt = take(static_cast<size_t>(n) * 2);
     L.rcnt = take(static_cast<size_t>(2) * n * 4);
-    L.rcur = take(static_cast<size_t>(2) * n * 4);
+    L.fpos = take(static_cast<size_t>(2) * n * p * 4);
     L.off = take(static_cast<size_t>(3) * (n + 1) * 8);
     L.rsrc = take(static_cast<size_t>(2) * n * p * 4);
     L.G = take(static_cast<size_t>(2) * n * cap * 4);
@@ -209,7 +210,7 @@ struct Run {
         S.fwd = reinterpret_cast<uint32_t*>(ws + L.fwd);
         S.fcnt = reinterpret_cast<uint8_t*>(ws + L.fcnt);
         S.rcnt = reinterpret_cast<uint32_t*>(ws + L.rcnt);
-        S.rcur = reinterpret_cast<uint32_t*>(ws + L.rcur);
+        S.fpos = reinterpret_cast<uint32_t*>(ws + L.fpos);
         S.off = reinterpret_cast<uint64_t*>(ws + L.off);
         S.rsrc = reinterpret_cast<uint32_t*>(ws + L.rsrc);
         S.G = reinterpret_cast<uint32_t*>(ws + L.G);
@@ -229,7 +230,6 @@ struct Run {
         if (c.err != cudaSuccess) return false;
         cudaMemsetAsync(G.bcnt, 0, static_cast<size_t>(D.n) * 4, c.stream);
         cudaMemsetAsync(S.rcnt, 0, static_cast<size_t>(2) * D.n * 4, c.stream);
-        cudaMemsetAsync(S.rcur, 0, static_cast<size_t>(2) * D.n * 4, c.stream);
         cudaMemsetAsync(stats, 0, sizeof(DevStats) * kMaxIters, c.stream);
         return true;
     }
@@ -302,7 +302,7 @@ struct Run {
         const int grid = warps_grid(D.n, wpb);
         DevStats* ps = prev_iter >= 0 ? stats + prev_iter : nullptr;
         c.launch(do_sample ? "k_merge_sample" : "k_merge", [&] {
-            k_merge_sample<<<grid, wpb * 32, wpb * 32 * sizeof(uint64_t), c.stream>>>(D, G, S, do_merge, do_sample, ps);
+            k_merge_sample<<<grid, wpb * 32, wpb * 64 * sizeof(uint64_t), c.stream>>>(D, G, S, do_merge, do_sample, ps);
         });
     }
 
@@ -374,6 +374,41 @@ struct Run {
                 constexpr size_t sm = LsCfg::kSmem;
                 cudaFuncSetAttribute(k_join_ls, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
                 k_join_ls<<<2 * sms, kLsThreads, sm, c.stream>>>(static_cast<const uint8_t*>(X), D, G, S, boundary, work, st);
+            });
+            return true;
+        }
+        const bool f32_tc = al && (metric == KNNG_COSINE || dt == KNNG_F32) && D.d % 4 == 0 && D.d <= 128;
+        if (f32_tc && jk == 4) {
+            // float rows: TF32 Gram tiles on the tensor cores, exact selection
+            // by canonical recomputation inside the error-bound window.  Opt-in:
+            // on DEEP-shaped rows it measured 36.6 ms per launch against 12.0 ms
+            // for the CUDA-core join (profiles/r01s2_ncu_k_join_tcf_deep.txt),
+            // so the automatic choice stays on k_join_ws for float rows.
+            const float* Xf = metric == KNNG_COSINE ? Xn : static_cast<const float*>(X);
+            float* sqn = reinterpret_cast<float*>(ws + L.sqn);
+            if (!sqn_ready) {
+                c.launch("k_sqnorm_f32", [&] {
+                    k_sqnorm_f32<<<static_cast<int>((D.n + 255) / 256), 256, 0, c.stream>>>(Xf, D.n, D.d, sqn);
+                });
+                sqn_ready = true;
+            }
+            unsigned long long* work = reinterpret_cast<unsigned long long*>(ws + L.flag + 8);
+            cudaMemsetAsync(work, 0, 8, c.stream);
+            c.launch("k_join", [&] {
+                const int ka = (D.d + 31) / 32;
+                const bool cs = metric == KNNG_COSINE;
+                auto go = [&](auto kfn, size_t sm, int ctas) {
+                    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+                    kfn<<<ctas * sms, kTcThreads, sm, c.stream>>>(Xf, sqn, D, G, S, boundary, work, st);
+                };
+                if (ka == 1) cs ? go(k_join_tcf<1, true>, TcfCfg<1>::kSmem, TcfCfg<1>::kCtas)
+                                : go(k_join_tcf<1, false>, TcfCfg<1>::kSmem, TcfCfg<1>::kCtas);
+                else if (ka == 2) cs ? go(k_join_tcf<2, true>, TcfCfg<2>::kSmem, TcfCfg<2>::kCtas)
+                                     : go(k_join_tcf<2, false>, TcfCfg<2>::kSmem, TcfCfg<2>::kCtas);
+                else if (ka == 3) cs ? go(k_join_tcf<3, true>, TcfCfg<3>::kSmem, TcfCfg<3>::kCtas)
+                                     : go(k_join_tcf<3, false>, TcfCfg<3>::kSmem, TcfCfg<3>::kCtas);
+                else cs ? go(k_join_tcf<4, true>, TcfCfg<4>::kSmem, TcfCfg<4>::kCtas)
+                        : go(k_join_tcf<4, false>, TcfCfg<4>::kSmem, TcfCfg<4>::kCtas);
             });
             return true;
         }
@@ -460,6 +495,7 @@ struct Run {
             s.appended = static_cast<int64_t>(h[i].appended);
             s.accepted = static_cast<int64_t>(h[i].accepted);
             s.rows = static_cast<int64_t>(h[i].rows);
+            s.recomputed = static_cast<int64_t>(h[i].recomputed);
             g_last_stats.push_back(s);
         }
     }
@@ -883,7 +919,7 @@ knng_status knng_set_option(const char* name, int64_t value) {
         return KNNG_OK;
     }
     if (strcmp(name, "join_kernel") == 0) {
-        if (value < 0 || value > 3) return fail(KNNG_E_USAGE, "join_kernel must be 0, 1, 2 or 3");
+        if (value < 0 || value > 4) return fail(KNNG_E_USAGE, "join_kernel must be 0, 1, 2, 3 or 4");
         g_opt_join_kernel.store(static_cast<int>(value));
         return KNNG_OK;
     }
@@ -899,6 +935,6 @@ knng_status knng_get_option(const char* name, int64_t* host_value) {
     return KNNG_OK;
 }
 
-int32_t knng_abi_version(void) { return 1; }
+int32_t knng_abi_version(void) { return 2; }
 
 }  // extern "C"

@@ -35,7 +35,7 @@ _STATUS = {0: "KNNG_OK", 1: "KNNG_E_USAGE", 2: "KNNG_E_DOMAIN", 3: "KNNG_E_NOMEM
 class IterStats(C.Structure):
     _fields_ = [("joins", C.c_int64), ("sum_m", C.c_int64), ("sum_q", C.c_int64),
                 ("dist_evals", C.c_int64), ("candidates", C.c_int64), ("appended", C.c_int64),
-                ("accepted", C.c_int64), ("rows", C.c_int64)]
+                ("accepted", C.c_int64), ("rows", C.c_int64), ("recomputed", C.c_int64)]
 
     def as_dict(self) -> dict:
         return {f: int(getattr(self, f)) for f, _ in self._fields_}

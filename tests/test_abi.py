@@ -28,7 +28,7 @@ def test_library_loads_and_exports_every_declared_symbol():
 
 
 def test_abi_version_and_status_strings():
-    assert K.knng_abi_version() == 1
+    assert K.knng_abi_version() == 2
     L = K.lib()
     assert L.knng_status_string(0) == b"KNNG_OK"
     assert L.knng_status_string(1) == b"KNNG_E_USAGE"
@@ -98,3 +98,11 @@ def test_launch_counter_and_timing_api_without_gpu():
     K.knng_reset_timing()
     assert K.knng_kernel_time("k_join") == (0.0, 0)
     K.knng_set_timing(False)
+
+
+def test_iter_stats_struct_matches_header():
+    hdr = open(os.path.join(ROOT, "include", "knng.h")).read()
+    body = hdr[hdr.index("typedef struct {"):hdr.index("} knng_iter_stats;")]
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    fields = re.findall(r"int64_t\s+(\w+);", body)
+    assert fields == [f for f, _ in K.IterStats._fields_]

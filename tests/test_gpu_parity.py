@@ -238,3 +238,35 @@ def test_legacy_join_kernel_matches(K):
         assert np.array_equal(gd.cpu().numpy(), od)
     finally:
         K.knng_set_option("join_kernel", 0)
+
+
+@pytest.mark.parametrize("jk", [0, 4])
+@pytest.mark.parametrize("shape,d,metric", [("deep", 96, "l2"), ("deep", 96, "cosine"), ("gist", 128, "l2"),
+                                            ("c1", 32, "l2"), ("gist", 60, "cosine")])
+def test_join_kernels_f32_match(K, jk, shape, d, metric):
+    """Float rows: the CUDA-core warp-specialised join (auto) and the opt-in
+    tensor-core join (4: TF32 Gram tile + canonical recomputation inside the
+    error-bound window) both give the oracle's graph bit for bit, in a
+    plain build and in a restricted (merge) run."""
+    m = _metric(metric)
+    X = datagen.make(shape, 5000, seed=12, d=d)
+    oi, od = orc.build(X, 16, 8, 5, 3, m)
+    nA = 2600
+    ia, da = orc.build(X[:nA], 16, 8, 3, 4, m)
+    ib, db = orc.build(X[nA:], 16, 8, 3, 5, m)
+    keys_in = np.concatenate([orc.key(da, ia), orc.key(db, ib.astype(np.uint64) + np.uint64(nA))])
+    expect = orc.merge(X, keys_in, nA, 16, 8, 3, 6, level=1, metric=m)
+    try:
+        K.knng_set_option("join_kernel", jk)
+        gi, gd = K.knng_build(dev(X), 16, 5, 8, 3, metric)
+        st = K.knng_last_stats()
+        assert np.array_equal(gi.cpu().numpy().view(np.uint32), oi)
+        assert np.array_equal(gd.cpu().numpy(), od)
+        if jk == 4:  # the window holds at least the selected key of every candidate
+            assert sum(s["recomputed"] for s in st) >= sum(s["candidates"] for s in st) > 0
+        mi, md = K.knng_merge(dev(X[:nA]), dev(ia.view(np.int32)), dev(da), dev(X[nA:]), dev(ib.view(np.int32)),
+                              dev(db), 16, 3, 8, seed=6, level=1, metric=metric)
+        assert np.array_equal(mi.cpu().numpy().view(np.uint32), orc.key_ids(expect))
+        assert np.array_equal(md.cpu().numpy(), orc.key_dists(expect))
+    finally:
+        K.knng_set_option("join_kernel", 0)

@@ -49,7 +49,9 @@ def main():
         st = K.knng_last_stats()
         print(json.dumps({"shape": a.shape, "n": n, "d": X.shape[1], "metric": a.metric,
                           "exact_u8": K.knng_get_option("last_exact_u8"), "ms_per_build": round(tot, 3),
-                          "kernels": per, "dist_evals": sum(s["dist_evals"] for s in st)}), flush=True)
+                          "kernels": per, "dist_evals": sum(s["dist_evals"] for s in st),
+                          "candidates": sum(s["candidates"] for s in st),
+                          "recomputed": sum(s.get("recomputed", 0) for s in st)}), flush=True)
         del X, ids, dists
         torch.cuda.empty_cache()
 
