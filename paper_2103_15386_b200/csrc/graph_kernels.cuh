@@ -308,6 +308,33 @@ __device__ __forceinline__ uint32_t warp_sort_unique_ids(uint32_t id, int& count
     return scratch[lane];
 }
 
+// D10 selection for r <= 32 reverse sources (one per lane in `src`): the c
+// = cap - fc smallest (Philox x0, s) keys go to lanes [fc, cap) of e.  Fast
+// path: sort u32 (x0 with its low 5 bits replaced by the lane), exact as long
+// as no two sources share the upper 27 bits of x0 -- then the order by those
+// bits is the order by (x0, s).  Returns true (e untouched) when such a tie
+// exists; the caller then runs the exact 64-bit path.
+__device__ __forceinline__ bool rev_select_ties(uint32_t src, int r, int f, uint32_t tword, int64_t v, uint2 key,
+                                                int fc, int c, uint32_t& e) {
+    const uint32_t lane = lane_id();
+    uint32_t pr = 0xFFFFFFFFu;
+    if (static_cast<int>(lane) < r) {
+        const uint4 o =
+            philox4x32_10(make_uint4(f == 0 ? kTagRevNew : kTagRevOld, tword, src, static_cast<uint32_t>(v)), key);
+        pr = (o.x & ~31u) | lane;
+    }
+    pr = warp_sort_u32(pr);
+    const uint32_t prev = __shfl_sync(kFull, pr, (lane + 31) & 31);
+    const bool tie = lane > 0 && static_cast<int>(lane) < r && (pr >> 5) == (prev >> 5);
+    if (__any_sync(kFull, tie)) return true;
+    const int j = static_cast<int>(lane) - fc;
+    const bool take = j >= 0 && j < c;
+    const uint32_t sel = __shfl_sync(kFull, pr, take ? j : 0);
+    const uint32_t id = __shfl_sync(kFull, src, sel & 31u);
+    if (take) e = id;
+    return false;
+}
+
 // One warp per node v: G(v) = sort_unique(F(v) U c smallest-priority reverse
 // sources), c = 2p - |F(v)| (P:149 cap 2p with the forward samples counted,
 // D8; priority key (Philox(tag, tword, s, v).x, s), D10; P:151 dedup), then
@@ -351,6 +378,8 @@ __global__ void k_rev_select(Dims D, Samples S, uint32_t tword, uint64_t seed) {
             const int j = static_cast<int>(lane) - fc;
             const uint32_t got = __shfl_sync(kFull, pre[f], j >= 0 && j < r ? j : 0);
             if (j >= 0 && j < r) e = got;
+        } else if (r <= 32 && !rev_select_ties(pre[f], r, f, tword, v, key, fc, c, e)) {
+            // selected by the 32-bit fast path (no priority ties)
         } else {
             uint64_t best = kSentinel;  // running 32 smallest (prio, s), sorted
             for (int base = 0; base < r; base += 32) {
@@ -362,8 +391,12 @@ __global__ void k_rev_select(Dims D, Samples S, uint32_t tword, uint64_t seed) {
                     x = (static_cast<uint64_t>(o.x) << 32) | src;
                 }
                 x = warp_sort_u64(x);
-                const uint64_t xr = shfl_u64(x, 31 - lane);
-                best = warp_bitonic_merge_u64(xr < best ? xr : best);
+                if (base == 0) {
+                    best = x;
+                } else {
+                    const uint64_t xr = shfl_u64(x, 31 - lane);
+                    best = warp_bitonic_merge_u64(xr < best ? xr : best);
+                }
             }
             const int j = static_cast<int>(lane) - fc;
             const uint64_t got = shfl_u64(best, j >= 0 && j < c ? j : 0);
