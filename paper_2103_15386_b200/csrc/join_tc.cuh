@@ -124,23 +124,6 @@ __device__ __forceinline__ uint32_t bit_range(int a, int b) {
     return hi & ~((1u << a) - 1u);
 }
 
-// L2 eviction-priority policies: the sample rows are re-read by many joins
-// (keep them: evict_last); sample lists and bucket appends stream through
-// (evict_first), so they do not push the rows out of L2.
-__device__ __forceinline__ uint64_t l2_policy_keep() {
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ uint64_t l2_policy_stream() {
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ void st_stream_u64(uint64_t* addr, uint64_t v, uint64_t pol) {
-    asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(addr), "l"(v), "l"(pol) : "memory");
-}
-
 __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
 k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Graph G, Samples S, int64_t boundary,
           unsigned long long* __restrict__ work, DevStats* __restrict__ stats) {
@@ -164,7 +147,6 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
     const int d = D.d, cap = D.cap;
     const bool restricted = boundary >= 0;
     const int kch = (d + 31) >> 5;  // MMAs of K = 32 (d % 16 == 0; zero-filled to 32)
-    const uint64_t pol_keep = l2_policy_keep(), pol_stream = l2_policy_stream();
 
     // ---------------------------------------------------------------- plans
     int cbuf = 1;
@@ -195,11 +177,9 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
                     const uint32_t* go = gn + static_cast<size_t>(D.n) * cap;
                     const uint32_t dn = smem_u32(cids + lane * 2 * cap), dq = dn + 4 * cap;
                     for (int c = 0; c < cap; c += 4) {
-                        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(dn + 4 * c),
-                                     "l"(gn + c), "l"(pol_stream)
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dn + 4 * c), "l"(gn + c)
                                      : "memory");
-                        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(dq + 4 * c),
-                                     "l"(go + c), "l"(pol_stream)
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dq + 4 * c), "l"(go + c)
                                      : "memory");
                     }
                 }
@@ -295,9 +275,9 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
             const uint8_t* src0 = X + part * 16;
             for (int slot = row0; slot < nslots; slot += 16) {
                 const uint32_t id = P.ids[slot];
-                asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
                                  dbase + slot * 128 + ((part ^ (slot & 7)) << 4)),
-                             "l"(src0 + static_cast<size_t>(id) * d), "l"(pol_keep)
+                             "l"(src0 + static_cast<size_t>(id) * d)
                              : "memory");
             }
         } else if (part < kchunks) {
@@ -331,7 +311,7 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
     auto file_store = [&]() {
 #pragma unroll
         for (int r = 0; r < 2; ++r)
-            if (f2_key[r] != kSentinel) st_stream_u64(G.bucket + f2_pos[r], f2_key[r], pol_stream);
+            if (f2_key[r] != kSentinel) G.bucket[f2_pos[r]] = f2_key[r];
     };
     auto file_atomic = [&]() {
         const bool ok0 = f1_key[0] < f1_th, ok1 = f1_key[1] < f1_th;  // D17 (the sentinel never passes)
