@@ -183,9 +183,9 @@ knng_status knng_debug_philox(const uint32_t* ctr, int64_t m, uint64_t seed,
  *                  (D5) yields, so the graph is bit-identical; SIFT-like data
  *                  qualifies.  0: always use the float path.
  *   "join_kernel"  0 (default): automatic -- the tensor-core join
- *                  (join_tc.cuh, exact int8 Gram tiles) for uint8 L2 rows
- *                  of d <= 128, d % 16 == 0, else the warp-specialised join
- *                  (join_ws.cuh);
+ *                  (join_tc.cuh, exact int8 Gram tiles; 8 epilogue warps, 3
+ *                  CTAs per SM) for uint8 L2 rows of d <= 128, d % 16 == 0,
+ *                  else the warp-specialised join (join_ws.cuh);
  *                  1: the batched cp.async join (join_kernel.cuh);
  *                  2: always the warp-specialised join;
  *                  3: the lock-step ALU join (join_ls.cuh) where the
@@ -194,7 +194,9 @@ knng_status knng_debug_philox(const uint32_t* ctr, int64_t m, uint64_t seed,
  *                     TF32 tensor-core join (join_tcf.cuh) -- exact
  *                     selection by canonical recomputation inside an
  *                     a-priori error window; slower than the CUDA-core
- *                     join on B200, so opt-in.
+ *                     join on B200, so opt-in;
+ *                  5: the tensor-core u8 join with 4 epilogue warps, 4 CTAs
+ *                     per SM; 6: 8 epilogue warps, 4 CTAs per SM.
  *                  All produce bit-identical graphs.
  *   "last_exact_u8" (read-only) 1 if the last build/merge on this thread ran
  *                  on the exact integer path.

@@ -68,7 +68,8 @@ struct TcCfg {
     static constexpr size_t kCacheCnt = 2 * 64;
     static constexpr size_t kCacheBytes = kCacheCnt + 2 * 32 * 2 * 32 * sizeof(uint32_t);
     static constexpr size_t kBarOff = (kCacheOff + kCacheBytes + 7) & ~size_t(7);
-    static constexpr size_t kUsed = kBarOff + 8 * (1 + 2 * kTcPlans) + 8;  // mbarriers + TMEM address
+    static constexpr size_t kCombOff = (kBarOff + 8 * (1 + 2 * kTcPlans) + 8 + 15) & ~size_t(15);
+    static constexpr size_t kUsed = kCombOff + 2 * kTcRows * 4;  // + upper-half partial minima (EPI = 8)
     static constexpr size_t kSmem = kUsed + 1024;  // + slack to align the rows to 1024 B
     static_assert(kTcCtasPerSm * (kSmem + 1024) <= 233472, "4 CTAs per SM");
 };
@@ -124,7 +125,12 @@ __device__ __forceinline__ uint32_t bit_range(int a, int b) {
     return hi & ~((1u << a) - 1u);
 }
 
-__global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
+// EPI epilogue warps: 4 (one thread per row), or 8 -- warps w and w + 4 read
+// the same TMEM lane quarter and split the row's column chunks, the upper
+// half handing its partial minima over through shared memory; 3 CTAs per SM
+// then keep 24 epilogue warps resident instead of 16.
+template <int EPI, int CTAS>
+__global__ void __launch_bounds__((EPI + 1) * 32, CTAS)
 k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Graph G, Samples S, int64_t boundary,
           unsigned long long* __restrict__ work, DevStats* __restrict__ stats) {
     extern __shared__ __align__(16) unsigned char tc_raw[];
@@ -140,10 +146,13 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
     uint64_t* plan_full = mma_bar + 1;             // [kTcPlans] planning warp -> warps 0-3
     uint64_t* plan_empty = plan_full + kTcPlans;   // [kTcPlans] warps 0-3 -> planning warp
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(plan_empty + kTcPlans);
+    int* comb = reinterpret_cast<int*>(tc_smem + TcCfg::kCombOff);
+    constexpr int PW = EPI;  // the planning warp
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const uint32_t lane = lane_id();
+    const bool upper = tid >= kTcRows;  // EPI = 8: second half of the row's columns
     const int d = D.d, cap = D.cap;
     const bool restricted = boundary >= 0;
     const int kch = (d + 31) >> 5;  // MMAs of K = 32 (d % 16 == 0; zero-filled to 32)
@@ -273,7 +282,7 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
         const uint32_t dbase = smem_u32(dst);
         if (part < nchunks) {
             const uint8_t* src0 = X + part * 16;
-            for (int slot = row0; slot < nslots; slot += 16) {
+            for (int slot = row0; slot < nslots; slot += EPI * 4) {
                 const uint32_t id = P.ids[slot];
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
                                  dbase + slot * 128 + ((part ^ (slot & 7)) << 4)),
@@ -281,7 +290,7 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
                              : "memory");
             }
         } else if (part < kchunks) {
-            for (int slot = row0; slot < nslots; slot += 16)
+            for (int slot = row0; slot < nslots; slot += EPI * 4)
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16, 0;\n" ::"r"(
                                  dbase + slot * 128 + ((part ^ (slot & 7)) << 4)),
                              "l"(X)
@@ -289,9 +298,11 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
         }
         cp_async_commit();
         // squared norm of slot tid's row (exact integer), staged as n * 128 + slot
-        const uint32_t id = P.ids[tid];
-        nv_next = id != 0xFFFFFFFFu ? __ldg(sqn + id) : 0;
-        side_next = __ballot_sync(kFull, id != 0xFFFFFFFFu && static_cast<int64_t>(id) >= boundary);
+        if (!upper) {
+            const uint32_t id = P.ids[tid];
+            nv_next = id != 0xFFFFFFFFu ? __ldg(sqn + id) : 0;
+            side_next = __ballot_sync(kFull, id != 0xFFFFFFFFu && static_cast<int64_t>(id) >= boundary);
+        }
     };
 
     // --------------------------------------------------------------- filing
@@ -338,7 +349,7 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
         mbar_init(mma_bar, 1);
         for (int i = 0; i < kTcPlans; ++i) {
             mbar_init(plan_full + i, 1);
-            mbar_init(plan_empty + i, kTcPlanWarp);
+            mbar_init(plan_empty + i, PW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -347,7 +358,7 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == kTcPlanWarp) {
+    if (warp == PW) {
         // ---- planning warp: runs up to kTcPlans batches ahead
         xnext = static_cast<int64_t>(__shfl_sync(kFull, claim(), 0));
         claimed = claim();
@@ -374,8 +385,10 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
                 cp_async_commit();
             }
             if (t == 0) {
-                nrm[tid] = nv_next * 128 + tid;
-                if (lane == 0) side[warp] = side_next;
+                if (!upper) {
+                    nrm[tid] = nv_next * 128 + tid;
+                    if (lane == 0) side[warp] = side_next;
+                }
             } else {
                 nv_prev = nv_next;
                 side_prev = side_next;
@@ -388,7 +401,7 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
             if (P.nnodes == 0) break;  // waited for at b - 2 (or in the prologue)
             cp_async_wait<1>();        // rows(b); rows(b+1) may be in flight
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // cp.async data -> MMA operand reads
-            named_bar(1, kTcPlanWarp * 32);  // rows(b), n'(b) visible; TMEM reads of b-1 done
+            named_bar(1, PW * 32);  // rows(b), n'(b) visible; TMEM reads of b-1 done
             if (tid == 0) {
                 tc_fence_after();
                 const uint32_t base = smem_u32(rows + buf * TcCfg::kRowBytes);
@@ -400,7 +413,7 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
             }
 
             // ---- my row of batch b
-            const int s = tid;
+            const int s = tid & (kTcRows - 1);
             const int nd = P.map[s];
             bool isNEW = false, isOLD = false;
             int sb = 0, m = 0, q = 0;
@@ -422,8 +435,10 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
             const int ns = nb[s] >> 7;  // n_s
             int minA = INT_MAX, minB = INT_MAX;
             // deferred filing of the two previous batches while MMA(b) runs
-            file_store();
-            file_atomic();
+            if (!upper) {
+                file_store();
+                file_atomic();
+            }
             mbar_wait(mma_bar, b & 1);
             tc_fence_after();
 
@@ -437,10 +452,15 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
             else cp_async_commit();
 
             // 16-column chunks over the warp's column range (the union of its
-            // rows' node ranges)
-            for (int cb = wlo & ~15; cb < whi; cb += 16) {
+            // rows' node ranges); EPI = 8 splits them between warps w, w + 4
+            const int c0 = wlo & ~15;
+            const int nchk = whi > c0 ? (whi - c0 + 15) >> 4 : 0;
+            const int half = EPI == 8 ? (nchk + 1) >> 1 : nchk;
+            const int cs = upper ? c0 + 16 * half : c0;
+            const int ce = upper ? whi : min(whi, c0 + 16 * half);
+            for (int cb = cs; cb < ce; cb += 16) {
                 uint32_t r[16];
-                tc_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + cb, r);
+                tc_ld16(tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + cb, r);
                 uint32_t A = act ? bit_range(sb - cb, sb + m - cb) : 0u;
                 if (isNEW && s >= cb && s < cb + 16) A &= ~(1u << (s - cb));
                 uint32_t B = isNEW ? bit_range(sb + m - cb, sb + m + q - cb) : 0u;
@@ -469,12 +489,23 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
                 }
             }
             tc_fence_before();
+            if constexpr (EPI == 8) {
+                if (upper) {
+                    comb[s] = minA;
+                    comb[kTcRows + s] = minB;
+                }
+                named_bar(2, PW * 32);
+                if (!upper) {
+                    minA = min(minA, comb[s]);
+                    minB = min(minB, comb[kTcRows + s]);
+                }
+            }
 
             // ---- this batch's keys (filed in iterations b+1 and b+2)
             uint64_t k1 = kSentinel, k2 = kSentinel;
-            if (act && minA != INT_MAX)
+            if (!upper && act && minA != INT_MAX)
                 k1 = make_key(static_cast<float>(ns + (minA >> 7)), P.ids[minA & 127]);
-            if (isNEW && minB != INT_MAX)
+            if (!upper && isNEW && minB != INT_MAX)
                 k2 = make_key(static_cast<float>(ns + (minB >> 7)), P.ids[minB & 127]);
             f1_key[0] = k1;
             f1_key[1] = k2;
@@ -487,16 +518,16 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
             // batch b+1's norms (their loads were issued one iteration ago);
             // buffer (b+1) % 3 was last read by the scans of b-2
             __syncwarp();
-            nrm[((b + 1) % 3) * kTcRows + tid] = nv_prev * 128 + tid;
+            if (!upper) nrm[((b + 1) % 3) * kTcRows + tid] = nv_prev * 128 + tid;
             nv_prev = nv_next;
             if (lane == 0) {
-                side[((b + 1) % 3) * 4 + warp] = side_prev;
+                if (!upper) side[((b + 1) % 3) * 4 + warp] = side_prev;
                 mbar_arrive(plan_empty + slot);  // this warp is done with plan b
             }
             side_prev = side_next;
         }
     }
-    if (warp < kTcPlanWarp) {
+    if (warp < PW && !upper) {
         file_store();
         file_atomic();
         file_store();
@@ -522,7 +553,7 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
         if (n_cand) atomicAdd(&stats->candidates, n_cand);
         if (n_app) atomicAdd(&stats->appended, n_app);
         if (my_pairs) atomicAdd(&stats->dist_evals, my_pairs);
-        if (warp == kTcPlanWarp && n_joins) {
+        if (warp == PW && n_joins) {
             atomicAdd(&stats->joins, n_joins);
             atomicAdd(&stats->sum_m, n_m);
             atomicAdd(&stats->sum_q, n_q);

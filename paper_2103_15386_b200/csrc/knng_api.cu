@@ -346,7 +346,7 @@ struct Run {
         }();
         (void)dbg_mode;
         const bool u8_slab = al && metric == KNNG_L2SQ && dt == KNNG_U8 && D.d <= kLsRow && D.d % 16 == 0;
-        if (u8_slab && jk == 0) {
+        if (u8_slab && (jk == 0 || jk == 5 || jk == 6)) {
             // uint8 rows of one 128-B slab: Gram tiles on the tensor cores
             int* sqn = reinterpret_cast<int*>(ws + L.sqn);
             if (!sqn_ready) {
@@ -360,9 +360,14 @@ struct Run {
             cudaMemsetAsync(work, 0, 8, c.stream);
             c.launch("k_join", [&] {
                 constexpr size_t sm = TcCfg::kSmem;
-                cudaFuncSetAttribute(k_join_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-                k_join_tc<<<kTcCtasPerSm * sms, kTcThreads, sm, c.stream>>>(static_cast<const uint8_t*>(X), sqn, D, G,
-                                                                           S, boundary, work, st);
+                auto go = [&](auto kfn, int ctas, int threads) {
+                    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+                    kfn<<<ctas * sms, threads, sm, c.stream>>>(static_cast<const uint8_t*>(X), sqn, D, G, S, boundary,
+                                                               work, st);
+                };
+                if (jk == 5) go(k_join_tc<4, 4>, 4, 5 * 32);       // 4 epilogue warps, 4 CTAs per SM
+                else if (jk == 6) go(k_join_tc<8, 4>, 4, 9 * 32);  // 8 epilogue warps, 4 CTAs per SM
+                else go(k_join_tc<8, 3>, 3, 9 * 32);               // 8 epilogue warps, 3 CTAs per SM
             });
             return true;
         }
@@ -919,7 +924,7 @@ knng_status knng_set_option(const char* name, int64_t value) {
         return KNNG_OK;
     }
     if (strcmp(name, "join_kernel") == 0) {
-        if (value < 0 || value > 4) return fail(KNNG_E_USAGE, "join_kernel must be 0, 1, 2, 3 or 4");
+        if (value < 0 || value > 6) return fail(KNNG_E_USAGE, "join_kernel must be in [0, 6]");
         g_opt_join_kernel.store(static_cast<int>(value));
         return KNNG_OK;
     }
