@@ -198,6 +198,14 @@ knng_status knng_debug_philox(const uint32_t* ctr, int64_t m, uint64_t seed,
  *                  5: the tensor-core u8 join with 4 epilogue warps, 4 CTAs
  *                     per SM; 6: 8 epilogue warps, 4 CTAs per SM.
  *                  All produce bit-identical graphs.
+ *   "join_order"   0 (default): node-id order; 1: the uint8 tensor-core
+ *                  join visits the nodes in a locality order (16-bit
+ *                  random-projection code, counting sort; order_kernels.cuh)
+ *                  so that nodes with overlapping sample sets run together.
+ *                  The result does not depend on it (bulk-synchronous
+ *                  update, D17).  Measured on C2: 2.66 -> 2.58 ms per join
+ *                  launch for ~1 ms of ordering per build -- no net gain,
+ *                  hence off.
  *   "last_exact_u8" (read-only) 1 if the last build/merge on this thread ran
  *                  on the exact integer path.
  * ---------------------------------------------------------------------- */

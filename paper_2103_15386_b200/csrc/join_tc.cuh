@@ -132,7 +132,7 @@ __device__ __forceinline__ uint32_t bit_range(int a, int b) {
 template <int EPI, int CTAS>
 __global__ void __launch_bounds__((EPI + 1) * 32, CTAS)
 k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Graph G, Samples S, int64_t boundary,
-          unsigned long long* __restrict__ work, DevStats* __restrict__ stats) {
+          unsigned long long* __restrict__ work, DevStats* __restrict__ stats, const uint32_t* __restrict__ perm) {
     extern __shared__ __align__(16) unsigned char tc_raw[];
     // rows need 1024-B alignment (SW128 atoms)
     unsigned char* tc_smem = tc_raw + ((1024 - (smem_u32(tc_raw) & 1023)) & 1023);
@@ -173,7 +173,18 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
     auto fetch = [&](int buf, int64_t xb) {
         if (xb < D.n) {
             const int nodes = static_cast<int>(D.n - xb < 32 ? D.n - xb : 32);
-            if (lane < 16) {
+            // node of chunk slot `lane`: xb + lane, or perm[xb + lane] (the
+            // locality order of order_kernels.cuh; needs cap % 4 == 0)
+            int64_t xl = xb + lane;
+            if (perm) {
+                uint32_t c2 = 0;
+                if (static_cast<int>(lane) < nodes) {
+                    xl = perm[xb + lane];
+                    c2 = *reinterpret_cast<const uint16_t*>(S.gcnt + 2 * xl);
+                }
+                cc_cnt[buf * 64 + 2 * lane] = static_cast<uint8_t>(c2);
+                cc_cnt[buf * 64 + 2 * lane + 1] = static_cast<uint8_t>(c2 >> 8);
+            } else if (lane < 16) {
                 const int lo = 4 * static_cast<int>(lane), bytes = max(0, min(4, 2 * nodes - lo));
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(smem_u32(cc_cnt + buf * 64 + lo)),
                              "l"(S.gcnt + 2 * xb + lo), "r"(bytes)
@@ -182,7 +193,7 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
             uint32_t* cids = cc_ids + static_cast<size_t>(buf) * 32 * 2 * cap;
             if ((cap & 3) == 0) {
                 if (static_cast<int>(lane) < nodes) {
-                    const uint32_t* gn = S.G + static_cast<size_t>(xb + lane) * cap;
+                    const uint32_t* gn = S.G + static_cast<size_t>(xl) * cap;
                     const uint32_t* go = gn + static_cast<size_t>(D.n) * cap;
                     const uint32_t dn = smem_u32(cids + lane * 2 * cap), dq = dn + 4 * cap;
                     for (int c = 0; c < cap; c += 4) {

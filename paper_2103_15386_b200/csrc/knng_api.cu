@@ -18,6 +18,7 @@
 #include "join_ls.cuh"
 #include "join_tc.cuh"
 #include "join_tcf.cuh"
+#include "order_kernels.cuh"
 #include "join_ws.cuh"
 
 using namespace knng;
@@ -30,6 +31,7 @@ std::atomic<int64_t> g_launches{0};
 std::atomic<int> g_timing{0};
 std::atomic<int> g_opt_exact_u8{1};
 std::atomic<int> g_opt_join_kernel{0};
+std::atomic<int> g_opt_join_order{0};
 thread_local int g_last_exact_u8 = 0;
 std::mutex g_time_mu;
 std::map<std::string, std::pair<double, int64_t>> g_times;
@@ -48,7 +50,7 @@ constexpr int kMaxIters = 256;
 
 // ---------------------------------------------------------------- layout
 struct Layout {
-    size_t keys, newmask, kth, bcnt, bucket, fwd, fcnt, rcnt, fpos, off, rsrc, G, gcnt, bsum, cand, stats,
+    size_t keys, newmask, kth, bcnt, bucket, fwd, fcnt, rcnt, fpos, off, osum, ocode, ohist, perm, rsrc, G, gcnt, bsum, cand, stats,
         xnorm, xu8, sqn, reserved, flag, total;
 };
 
@@ -86,6 +88,10 @@ Layout make_layout(int64_t n, int d, int k, int p, bool cosine, bool own_keys, b
     L.reserved = merge ? take(static_cast<size_t>(n) * (k / 2 > 0 ? k / 2 : 1) * 8) : 0;
     L.xu8 = u8copy ? take(static_cast<size_t>(n) * d) : 0;  // exact integer copy (option exact_u8)
     L.sqn = take(static_cast<size_t>(n) * 4);                // exact squared norms (uint8 tensor-core join)
+    L.osum = take(static_cast<size_t>(d) * 4);               // join order: column sums,
+    L.ocode = take(static_cast<size_t>(n) * 4);              //   projection codes,
+    L.ohist = take(static_cast<size_t>(kOrderBuckets) * 4);  //   bucket offsets,
+    L.perm = take(static_cast<size_t>(n) * 4);               //   node order
     L.flag = take(16);
     L.total = off;
     return L;
@@ -196,7 +202,8 @@ struct Run {
     const float* Xn;
     uint64_t seed;
     int64_t boundary = -1;
-    bool sqn_ready = false;  // L.sqn holds the exact squared norms of X
+    bool sqn_ready = false;   // L.sqn holds the exact squared norms of X
+    bool perm_ready = false;  // L.perm holds the join order
 
     Run(Ctx& ctx) : c(ctx) {}
 
@@ -356,14 +363,35 @@ struct Run {
                 });
                 sqn_ready = true;
             }
+            if (!perm_ready && g_opt_join_order.load() && D.cap % 4 == 0 && D.d <= kOrderMaxD) {
+                // locality order of the joins (performance only, D17)
+                float* osum = reinterpret_cast<float*>(ws + L.osum);
+                uint32_t* ocode = reinterpret_cast<uint32_t*>(ws + L.ocode);
+                uint32_t* ohist = reinterpret_cast<uint32_t*>(ws + L.ohist);
+                uint32_t* operm = reinterpret_cast<uint32_t*>(ws + L.perm);
+                cudaMemsetAsync(osum, 0, static_cast<size_t>(D.d) * 4, c.stream);
+                cudaMemsetAsync(ohist, 0, static_cast<size_t>(kOrderBuckets) * 4, c.stream);
+                const uint8_t* Xu = static_cast<const uint8_t*>(X);
+                const int nb = static_cast<int>((D.n + 255) / 256);
+                c.launch("k_order_colsum",
+                         [&] { k_order_colsum<uint8_t><<<8 * sms, 128, 0, c.stream>>>(Xu, D.n, D.d, osum); });
+                c.launch("k_order_code", [&] {
+                    k_order_code<uint8_t><<<nb, 256, 0, c.stream>>>(Xu, D.n, D.d, osum, ocode, ohist);
+                });
+                c.launch("k_order_scan", [&] { k_order_scan<<<1, 256, 0, c.stream>>>(ohist); });
+                c.launch("k_order_scatter",
+                         [&] { k_order_scatter<<<nb, 256, 0, c.stream>>>(ocode, D.n, ohist, operm); });
+                perm_ready = true;
+            }
             unsigned long long* work = reinterpret_cast<unsigned long long*>(ws + L.flag + 8);
             cudaMemsetAsync(work, 0, 8, c.stream);
             c.launch("k_join", [&] {
                 constexpr size_t sm = TcCfg::kSmem;
+                const uint32_t* pm = perm_ready ? reinterpret_cast<const uint32_t*>(ws + L.perm) : nullptr;
                 auto go = [&](auto kfn, int ctas, int threads) {
                     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
                     kfn<<<ctas * sms, threads, sm, c.stream>>>(static_cast<const uint8_t*>(X), sqn, D, G, S, boundary,
-                                                               work, st);
+                                                               work, st, pm);
                 };
                 if (jk == 5) go(k_join_tc<4, 4>, 4, 5 * 32);       // 4 epilogue warps, 4 CTAs per SM
                 else if (jk == 6) go(k_join_tc<8, 4>, 4, 9 * 32);  // 8 epilogue warps, 4 CTAs per SM
@@ -923,6 +951,10 @@ knng_status knng_set_option(const char* name, int64_t value) {
         g_opt_exact_u8.store(value ? 1 : 0);
         return KNNG_OK;
     }
+    if (strcmp(name, "join_order") == 0) {
+        g_opt_join_order.store(value ? 1 : 0);
+        return KNNG_OK;
+    }
     if (strcmp(name, "join_kernel") == 0) {
         if (value < 0 || value > 6) return fail(KNNG_E_USAGE, "join_kernel must be in [0, 6]");
         g_opt_join_kernel.store(static_cast<int>(value));
@@ -935,6 +967,7 @@ knng_status knng_get_option(const char* name, int64_t* host_value) {
     if (!name || !host_value) return fail(KNNG_E_USAGE, "null argument");
     if (strcmp(name, "exact_u8") == 0) *host_value = g_opt_exact_u8.load();
     else if (strcmp(name, "join_kernel") == 0) *host_value = g_opt_join_kernel.load();
+    else if (strcmp(name, "join_order") == 0) *host_value = g_opt_join_order.load();
     else if (strcmp(name, "last_exact_u8") == 0) *host_value = g_last_exact_u8;
     else return fail(KNNG_E_USAGE, "unknown option '%s'", name);
     return KNNG_OK;

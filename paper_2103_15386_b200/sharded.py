@@ -98,12 +98,14 @@ class _Comm:
             self.dist.recv(t, src, group=self.group)
 
 
-def knng_build_sharded(local_vectors, shards: int, k: int, iters: int, merge_iters: int, sample_size: int,
+def knng_build_sharded(local_vectors, shards: int, k: int, iters: int, merge_iters, sample_size: int,
                        seed: int = 0, metric="l2", group=None, ops=None, scatter: bool = True, timeline=None):
     """GNND on every shard + log-depth GGM tree across ranks.
 
     local_vectors: this rank's rows [n_local, d], n_local = shard_rows * S/P
-    (all ranks equal).  Returns (ids int32 [n_local, k] with GLOBAL ids,
+    (all ranks equal).  merge_iters: one count for every level, or a
+    sequence with one count per tree level (D23: higher levels merge larger
+    sets and need more refine iterations).  Returns (ids int32 [n_local, k] with GLOBAL ids,
     dists float32) when scatter, else the whole graph on rank 0 and None on
     the other ranks.  timeline: optional list receiving (phase, level) marks
     (host-side order of events, for tests)."""
@@ -120,6 +122,12 @@ def knng_build_sharded(local_vectors, shards: int, k: int, iters: int, merge_ite
     ns = n_local // per
     steps = plan(shards, world)
     dev = local_vectors.device
+    if isinstance(merge_iters, int):
+        level_iters = [merge_iters] * len(steps)
+    else:
+        level_iters = [int(m) for m in merge_iters]
+        if len(level_iters) < len(steps):
+            raise ValueError(f"merge_iters needs one count per level ({len(steps)})")
 
     # Vectors of the largest block this rank leads, local rows first: a
     # received right half lands right after the left half, so merged blocks
@@ -171,8 +179,8 @@ def knng_build_sharded(local_vectors, shards: int, k: int, iters: int, merge_ite
                 else:
                     ib, db = blocks.pop(gB)
                     loB = (gB - first) * ns
-                blocks[gA] = ops.merge(X[loA:loA + rows], ia, da, X[loB:loB + rows], ib, db, k, merge_iters,
-                                       sample_size, seed, s.level, metric)
+                blocks[gA] = ops.merge(X[loA:loA + rows], ia, da, X[loB:loB + rows], ib, db, k,
+                                       level_iters[s.level], sample_size, seed, s.level, metric)
                 if timeline is not None:
                     timeline.append(("merge", s.level))
 

@@ -270,3 +270,18 @@ def test_join_kernels_f32_match(K, jk, shape, d, metric):
         assert np.array_equal(md.cpu().numpy(), orc.key_dists(expect))
     finally:
         K.knng_set_option("join_kernel", 0)
+
+
+def test_join_order_does_not_change_the_graph(K):
+    """The locality order of the joins (option join_order) is a performance
+    device only: the bulk-synchronous update is order-independent (D17)."""
+    X = datagen.make("sift", 6000, seed=13, dtype="u8")
+    oi, od = orc.build(X, 32, 16, 5, 7)
+    try:
+        for jo in (0, 1):
+            K.knng_set_option("join_order", jo)
+            gi, gd = K.knng_build(dev(X), 32, 5, 16, 7)
+            assert np.array_equal(gi.cpu().numpy().view(np.uint32), oi)
+            assert np.array_equal(gd.cpu().numpy(), od)
+    finally:
+        K.knng_set_option("join_order", 0)

@@ -14,7 +14,8 @@ import paper_2103_15386_b200.knng as K  # noqa: E402
 
 NAMES = ["k_init", "k_merge_sample", "k_scan_reduce", "k_scan_bsums", "k_scan_final", "k_rev_scatter",
          "k_rev_select", "k_join", "k_cand_scatter", "k_export", "k_check_u8", "k_to_u8", "k_normalize",
-         "k_sqnorm_u8", "k_ggm_seed", "k_ggm_finalize"]
+         "k_sqnorm_u8", "k_ggm_seed", "k_ggm_finalize", "k_order_colsum", "k_order_code", "k_order_scan",
+         "k_order_scatter", "k_sqnorm_f32"]
 
 
 def main():
