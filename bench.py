@@ -51,8 +51,9 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=20_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--merge-iters", type=int, default=6,
-                    help="GGM refine iterations per tree level (N>1, and the N=1 GGM line)")
+    ap.add_argument("--merge-iters", default="6",
+                    help="GGM refine iterations: one count, or one per tree level (N>1); the N=1 GGM "
+                         "line uses the first")
     ap.add_argument("--no-ggm", action="store_true", help="skip the N=1 GGM measurement")
     return ap.parse_args()
 
@@ -122,12 +123,15 @@ class ClockSampler:
 
 def workload(args, rank, world=1):
     """N=1: the C2 SIFT1M-shaped set.  N>1: shard `rank` of an N x 1M
-    SIFT-shaped set (one mixture with 1000 N components, rows from the
-    stream (1, rank)) -- the sharded build's weak-scaling workload."""
+    SIFT-shaped set (one mixture of 1000 components, rows from the stream
+    (1, rank)) -- the sharded build's weak-scaling workload.  Every shard
+    holds ~1000 rows of every component, as the C2 set does: the GGM merge
+    navigates the shard graphs from random cross seeds and needs components
+    that are not split into tiny per-shard islands (D38)."""
     import datagen
     if world == 1:
         return datagen.make("sift", args.n, seed=1)
-    return datagen.make("sift", args.n, seed=1, part=rank, components=1000 * world)
+    return datagen.make("sift", args.n, seed=1, part=rank, components=1000)
 
 
 def cpu_baseline(args, X) -> dict:
@@ -199,7 +203,7 @@ def measure_ggm(args, K, Xd, stream):
                      dtype=torch.uint8, device="cuda")
 
     def merge():
-        return K.knng_merge(XA, ia, da, XB, ib, db, args.k, args.merge_iters, args.p, seed=args.seed, level=0,
+        return K.knng_merge(XA, ia, da, XB, ib, db, args.k, args.merge_iters[0], args.p, seed=args.seed, level=0,
                             workspace=ws, stream=stream)
 
     for _ in range(2):
@@ -220,7 +224,7 @@ def measure_ggm(args, K, Xd, stream):
     st = K.knng_last_stats()
     rec, nq = recall_at_10(K, Xd, md, args.recall_nodes)
     return {"workload": f"C2 split into 2 x {h} (knng_build per half, seeds {args.seed}/{args.seed + 1}), "
-                        f"then knng_merge", "merge_iters": args.merge_iters, "ms_per_merge": ms,
+                        f"then knng_merge", "merge_iters": args.merge_iters[0], "ms_per_merge": ms,
             "recall_at_10": rec, "recall_nodes": nq,
             "join_ms_per_launch": join_ms / max(1, join_launches),
             "dist_evals": sum(s["dist_evals"] for s in st), "accepted": sum(s["accepted"] for s in st),
@@ -229,6 +233,7 @@ def measure_ggm(args, K, Xd, stream):
 
 def main():
     args = parse()
+    args.merge_iters = [int(m) for m in str(args.merge_iters).split(",")]
     if args.impl == "reference":
         run_reference(args)
         return
@@ -295,13 +300,15 @@ def main():
 
     ops = Ops(stream=stream)
     out = {}
+    levels = max(0, world.bit_length() - 1)  # log2(world) tree levels (world a power of two)
+    level_iters = [args.merge_iters[min(i, len(args.merge_iters) - 1)] for i in range(levels)]
 
     def step():
         if world == 1:
             K.knng_build(Xd, args.k, args.iters, args.p, args.seed, "l2", ids, dists, ws, stream)
             ops.history.extend(K.knng_last_stats())
         else:  # one shard per GPU, log-depth GGM tree over NCCL (sharded.py)
-            out["g"] = knng_build_sharded(Xd, world, args.k, args.iters, args.merge_iters, args.p, args.seed,
+            out["g"] = knng_build_sharded(Xd, world, args.k, args.iters, level_iters, args.p, args.seed,
                                           ops=ops)
 
     for _ in range(max(3, args.warmup)):
@@ -359,7 +366,7 @@ def main():
                     raise RuntimeError(K.knng_last_error())
             else:
                 Xd.copy_(Xh, non_blocking=True)
-                gi, gd = knng_build_sharded(Xd, world, args.k, args.iters, args.merge_iters, args.p, args.seed,
+                gi, gd = knng_build_sharded(Xd, world, args.k, args.iters, level_iters, args.p, args.seed,
                                             ops=CudaOps(stream=stream))
                 ih.copy_(gi, non_blocking=True)
                 dh.copy_(gd, non_blocking=True)
@@ -431,10 +438,11 @@ def main():
                    "sample_size": args.p, "iters": args.iters, "metric": "l2",
                    "l2_flush": "inputs (512 MB) larger than L2"}
         else:
-            cfg = {"workload": f"sharded SIFT-shaped {world} x {n} (one 1M shard per GPU, log-depth GGM tree "
-                               f"over NCCL; C4/C5 scheme at C2 shard size)", "n": world * n, "n_per_gpu": n,
+            cfg = {"workload": f"sharded SIFT-shaped {world} x {n} (one {n}-row shard per GPU, GNND per shard + "
+                               f"log-depth GGM tree over NCCL: the C4/C5 scheme at C2 shard size)",
+                   "n": world * n, "n_per_gpu": n,
                    "d": d, "k": args.k, "sample_size": args.p, "iters": args.iters,
-                   "merge_iters": args.merge_iters, "shards": world, "metric": "l2",
+                   "merge_iters": level_iters, "shards": world, "metric": "l2",
                    "l2_flush": "inputs (512 MB per GPU) larger than L2"}
         line = {"metric": METRIC, "value": ms / 1000.0, "unit": "s", "n_gpus": world, "steps": args.steps,
                 "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",

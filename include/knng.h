@@ -125,6 +125,18 @@ knng_status knng_merge(const void* vecA, int64_t nA, const uint32_t* idsA,
                        size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------------------------
+ * Sharded build (D26, D36, section 11).  There is no
+ * separate C entry point: the multi-GPU build is knng_build on every shard
+ * (shard g of S built with seed + g, local ids) followed by knng_merge per
+ * tree level (level l merges groups of 2^(l+1) shards, ids numbered from the
+ * group's first row, Philox level l).  The exchange between GPUs is one
+ * point-to-point block transfer (vectors, ids, dists) per level, done by
+ * paper_2103_15386_b200/sharded.py over torch.distributed (NCCL on NVLink);
+ * knng_merge uses the received rows in place when they follow the leader's
+ * own (D37).  The result depends only on S, not on the number of GPUs.
+ * ---------------------------------------------------------------------- */
+
+/* ------------------------------------------------------------------------
  * knng_bruteforce -- exact top-kq neighbours (j != q) of nq query rows by
  * exhaustive scan, for recall@10 ground truth (Eq. 4).
  *   queries [nq] device int64 row ids; out_ids/out_dists [nq][kq] device.

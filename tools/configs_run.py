@@ -44,8 +44,9 @@ def gen(shape, n, parts, dtype="f32"):
     t0 = time.time()
     per = n // parts
     # components: SURVEY.md section 8(d) -- SIFT-like 1000 per 10^6 rows;
-    # DEEP: 10^4 for the whole DEEP100M set (a subsample keeps that count)
-    comps = 10_000 if shape == "deep" else datagen.SHAPES[shape][1] * max(1, n // 1_000_000)
+    # DEEP100M: 10^4 components for 10^8 rows, i.e. 10^4 rows per component
+    # (kept at smaller n, so every shard sees >= 1250 rows of a component)
+    comps = max(1, n // 10_000) if shape == "deep" else datagen.SHAPES[shape][1] * max(1, n // 1_000_000)
     X = np.concatenate([datagen.make(shape, per, seed=1, part=i, components=comps, dtype=dtype)
                         for i in range(parts)])
     return torch.from_numpy(X).cuda(), time.time() - t0

@@ -23,9 +23,11 @@ ap.add_argument("--mi", default="6,10,14")
 ap.add_argument("--iters", type=int, default=10)
 ap.add_argument("--k", type=int, default=32)
 ap.add_argument("--p", type=int, default=16)
+ap.add_argument("--comps", type=int, default=0)
 a = ap.parse_args()
 per = a.n // a.parts
-comps = 10_000 if a.shape == "deep" else datagen.SHAPES[a.shape][1] * max(1, a.n // 1_000_000)
+ap2 = a.n // 10_000 if a.shape == "deep" else datagen.SHAPES[a.shape][1] * max(1, a.n // 1_000_000)
+comps = a.comps or ap2
 X = torch.from_numpy(np.concatenate([datagen.make(a.shape, per, seed=1, part=i, components=comps)
                                      for i in range(a.parts)])).cuda()
 q = datagen.sample_nodes(a.n, 10000)
