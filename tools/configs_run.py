@@ -44,9 +44,10 @@ def gen(shape, n, parts, dtype="f32"):
     t0 = time.time()
     per = n // parts
     # components: SURVEY.md section 8(d) -- SIFT-like 1000 per 10^6 rows;
-    # DEEP100M: 10^4 components for 10^8 rows, i.e. 10^4 rows per component
-    # (kept at smaller n, so every shard sees >= 1250 rows of a component)
-    comps = max(1, n // 10_000) if shape == "deep" else datagen.SHAPES[shape][1] * max(1, n // 1_000_000)
+    # DEEP100M: 10^4 components for 10^8 rows, SIFT1B: 10^5 for 10^9, i.e.
+    # 10^4 rows per component (kept at smaller n, so every shard of 8 sees
+    # ~1250 rows of a component; D38)
+    comps = max(1, n // 10_000) if (shape == "deep" or dtype == "u8") else datagen.SHAPES[shape][1] * max(1, n // 1_000_000)
     X = np.concatenate([datagen.make(shape, per, seed=1, part=i, components=comps, dtype=dtype)
                         for i in range(parts)])
     return torch.from_numpy(X).cuda(), time.time() - t0
@@ -59,6 +60,7 @@ def main():
     ap.add_argument("--shards", type=int, default=8)
     ap.add_argument("--iters", default="7", help="comma list: every value is measured")
     ap.add_argument("--merge-iters", type=int, default=6)
+    ap.add_argument("--p", type=int, default=None, help="sample size (default: 16 for c3/c4, 8 for c5)")
     ap.add_argument("--no-tree", action="store_true")
     a = ap.parse_args()
     out = []
@@ -76,6 +78,7 @@ def main():
     else:
         c4 = a.config == "c4"
         shape, k, p = ("deep", 32, 16) if c4 else ("sift", 16, 8)
+        p = a.p or p
         n = a.n or (8_000_000 if c4 else 8_000_000)
         X, gs = gen(shape, n, a.shards, "f32" if c4 else "u8")
         name = "C4 DEEP-shaped" if c4 else "C5 SIFT-shaped uint8"
@@ -89,6 +92,7 @@ def main():
             del di, dd
         if not a.no_tree:
             it = its[-1]
+            knng_build_sharded(X, a.shards, k, 1, 1, p, 42)  # warm-up (pools, kernel attributes)
             (ids, d), ms = timed(lambda: knng_build_sharded(X, a.shards, k, it, a.merge_iters, p, 42))
             print(json.dumps({"config": name, "mode": f"tree of {a.shards} shards (one GPU)", "n": n,
                               "d": X.shape[1], "k": k, "p": p, "iters": it, "merge_iters": a.merge_iters,
