@@ -221,6 +221,12 @@ def measure_ggm(args, K, Xd, stream):
     K.knng_set_timing(False)
     ms = e0.elapsed_time(e1) / reps
     join_ms, join_launches = K.knng_kernel_time("k_join")
+    kernels = {}
+    for nm in ["k_ggm_seed", "k_merge_sample", "k_rev_scatter", "k_rev_select", "k_join", "k_ggm_finalize",
+               "k_check_u8", "k_to_u8", "k_export"]:
+        t, c = K.knng_kernel_time(nm)
+        if c:
+            kernels[nm] = round(t / reps, 3)
     st = K.knng_last_stats()
     rec, nq = recall_at_10(K, Xd, md, args.recall_nodes)
     return {"workload": f"C2 split into 2 x {h} (knng_build per half, seeds {args.seed}/{args.seed + 1}), "
@@ -228,7 +234,8 @@ def measure_ggm(args, K, Xd, stream):
             "recall_at_10": rec, "recall_nodes": nq,
             "join_ms_per_launch": join_ms / max(1, join_launches),
             "dist_evals": sum(s["dist_evals"] for s in st), "accepted": sum(s["accepted"] for s in st),
-            "dist_evals_per_s": sum(s["dist_evals"] for s in st) / (ms * 1e-3)}
+            "dist_evals_per_s": sum(s["dist_evals"] for s in st) / (ms * 1e-3),
+            "kernel_ms_per_merge": kernels}
 
 
 def main():

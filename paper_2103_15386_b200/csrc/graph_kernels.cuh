@@ -109,27 +109,19 @@ __global__ void k_merge_sample(Dims D, Graph G, Samples S, int do_merge, int do_
     const uint32_t lane = lane_id();
     const int k = D.k, p = D.p;
     const bool in_list = static_cast<int>(lane) < k;
-    // independent loads first: mask, list, bucket count and offset, and the
-    // first 32 bucket entries (bounded by the bucket's capacity, D34)
     const uint32_t mask = G.newmask[s];
-    Elem cur{in_list ? G.keys[static_cast<size_t>(s) * k + lane] : kSentinel, 0u};
+    Elem cur{in_list ? G.keys[static_cast<size_t>(s) * k + lane] : kSentinel,
+             in_list ? ((mask >> lane) & 1u) : 0u};
     bool changed = false;
-    uint32_t c = 0;
-    uint64_t cand0 = kSentinel;
-    const uint64_t* bk = nullptr;
     if (do_merge) {
-        c = G.bcnt[s];
-        bk = G.bucket + G.boff[s];
-        if (lane < c) cand0 = bk[lane];
-    }
-    cur.meta = in_list ? ((mask >> lane) & 1u) : 0u;
-    if (do_merge) {
+        const uint32_t c = G.bcnt[s];
         if (c > 0) {
             extern __shared__ uint64_t ms_scratch[];  // 64 u64 per warp: scratch, list copy
             uint64_t* scr = ms_scratch + (threadIdx.x >> 5) * 64;
             uint64_t* lst = scr + 32;
+            const uint64_t* bk = G.bucket + G.boff[s];
             for (uint32_t base = 0; base < c; base += 32) {
-                const uint64_t cand = base == 0 ? cand0 : ((base + lane < c) ? bk[base + lane] : kSentinel);
+                const uint64_t cand = (base + lane < c) ? bk[base + lane] : kSentinel;
                 // Pre-filter (exact): a candidate equal to a list key is the
                 // same id (D5 keys are canonical per id) and one not below the
                 // current k-th key cannot enter the k smallest.  Only the
