@@ -505,7 +505,7 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
                     comb[s] = minA;
                     comb[kTcRows + s] = minB;
                 }
-                named_bar(2, PW * 32);
+                named_bar(2 + (warp & 3), 64);  // the pair (w, w + 4) only
                 if (!upper) {
                     minA = min(minA, comb[s]);
                     minB = min(minB, comb[kTcRows + s]);
