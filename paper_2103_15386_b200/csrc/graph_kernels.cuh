@@ -339,7 +339,7 @@ __device__ __forceinline__ bool rev_select_ties(uint32_t src, int r, int f, uint
 // sources), c = 2p - |F(v)| (P:149 cap 2p with the forward samples counted,
 // D8; priority key (Philox(tag, tword, s, v).x, s), D10; P:151 dedup), then
 // G_old(v) minus G_new(v) (D11).  Requires 2p <= 32.
-__global__ void __launch_bounds__(256, 6) k_rev_select(Dims D, Samples S, uint32_t tword, uint64_t seed) {
+__global__ void __launch_bounds__(256, 8) k_rev_select(Dims D, Samples S, uint32_t tword, uint64_t seed) {
     const int64_t v = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (v >= D.n) return;
     const uint32_t lane = lane_id();
