@@ -151,3 +151,31 @@ def test_gpu_sharded_two_ranks_equals_oracle_tree(tmp_path):
     _, expect = _expected()
     got = _run_world(2, True, tmp_path)
     assert np.array_equal(got, expect)
+
+
+@pytest.mark.gpu
+def test_gpu_sharded_medium_eight_shards_equals_oracle_tree():
+    # 8 shards x 4000 rows (3 tree levels, many join batches per level): the
+    # libknng tree equals the oracle's tree_build bit for bit
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    X = datagen.make("c1", 32000, seed=21)
+    k, p, iters, mi, seed = 10, 8, 6, 5, 9
+    expect = orc.tree_build(X, 8, k, p, iters, mi, seed)
+    ids, dists = knng_build_sharded(torch.from_numpy(X).cuda(), 8, k, iters, mi, p, seed)
+    got = orc.key(dists.cpu().numpy(), ids.cpu().numpy().view(np.uint32))
+    assert np.array_equal(got, expect)
+    # per-level merge iterations (D23): same as the oracle with the same count per level
+    ids2, dists2 = knng_build_sharded(torch.from_numpy(X).cuda(), 8, k, iters, [mi, mi, mi], p, seed)
+    assert np.array_equal(ids2.cpu().numpy(), ids.cpu().numpy())
+
+
+def test_sharded_per_level_merge_iters():
+    X, _ = _expected()
+    with pytest.raises(ValueError):
+        knng_build_sharded(torch.from_numpy(X), 4, CASE["k"], 2, [1], CASE["p"], CASE["seed"], ops=OracleOps())
+    # a list with one count per level equals the oracle tree with that count
+    ids, dists = knng_build_sharded(torch.from_numpy(X), 4, CASE["k"], CASE["iters"],
+                                    [CASE["merge_iters"]] * 2, CASE["p"], CASE["seed"], ops=OracleOps())
+    _, expect = _expected()
+    assert np.array_equal(orc.key(dists.numpy(), ids.numpy().view(np.uint32)), expect)
