@@ -52,6 +52,7 @@ constexpr int kMaxIters = 256;
 struct Layout {
     size_t keys, newmask, kth, bcnt, bucket, fwd, fcnt, rcnt, fpos, off, osum, ocode, ohist, perm, rsrc, G, gcnt, bsum, cand, stats,
         xnorm, xu8, sqn, reserved, flag, total;
+    bool has_cand;
 };
 
 int64_t scan_blocks(int64_t n) { return (n + kScanBlock - 1) / kScanBlock; }
@@ -82,7 +83,11 @@ Layout make_layout(int64_t n, int d, int k, int p, bool cosine, bool own_keys, b
     L.G = take(static_cast<size_t>(2) * n * cap * 4);
     L.gcnt = take(static_cast<size_t>(n) * 2);
     L.bsum = take(static_cast<size_t>(3) * scan_blocks(n) * 8);
-    L.cand = take(static_cast<size_t>(n) * 3 * cap * 8);
+    // join output staging: only the legacy batched join (option join_kernel 1,
+    // or rows that are not whole 16-B chunks) files through it; the other joins
+    // file inside the kernel.  (A misaligned base pointer allocates it lazily.)
+    L.has_cand = g_opt_join_kernel.load() == 1 || d % 16 != 0;
+    L.cand = L.has_cand ? take(static_cast<size_t>(n) * 3 * cap * 8) : 0;
     L.stats = take(sizeof(DevStats) * kMaxIters);
     L.xnorm = cosine ? take(static_cast<size_t>(n) * d * 4) : 0;
     L.reserved = merge ? take(static_cast<size_t>(n) * (k / 2 > 0 ? k / 2 : 1) * 8) : 0;
@@ -104,6 +109,7 @@ struct Ctx {
     std::vector<cudaEvent_t> pool;
     std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
     void* owned_ws = nullptr;
+    void* owned_extra = nullptr;  // lazily allocated join staging (misaligned rows)
     cudaError_t err = cudaSuccess;
     std::string err_where;
 
@@ -116,6 +122,7 @@ struct Ctx {
     ~Ctx() {
         for (auto e : pool) cudaEventDestroy(e);
         if (owned_ws) cudaFreeAsync(owned_ws, stream);
+        if (owned_extra) cudaFreeAsync(owned_extra, stream);
     }
     // launch bookkeeping: count, optional events, error capture
     template <typename F>
@@ -223,7 +230,7 @@ struct Run {
         S.G = reinterpret_cast<uint32_t*>(ws + L.G);
         S.gcnt = reinterpret_cast<uint8_t*>(ws + L.gcnt);
         S.bsum = reinterpret_cast<uint64_t*>(ws + L.bsum);
-        S.cand = reinterpret_cast<uint64_t*>(ws + L.cand);
+        S.cand = L.has_cand ? reinterpret_cast<uint64_t*>(ws + L.cand) : nullptr;
         G.boff = S.off + 2 * (D.n + 1);
         stats = reinterpret_cast<DevStats*>(ws + L.stats);
         Xn = metric == KNNG_COSINE ? reinterpret_cast<const float*>(ws + L.xnorm) : nullptr;
@@ -469,6 +476,17 @@ struct Run {
                 }
             });
             return true;
+        }
+        if (!S.cand) {  // legacy join on rows the workspace did not plan it for
+            void* p = nullptr;
+            if (cudaMallocAsync(&p, static_cast<size_t>(D.n) * 3 * D.cap * 8, c.stream) != cudaSuccess) {
+                cudaGetLastError();
+                c.err = cudaErrorMemoryAllocation;
+                c.err_where = "join staging allocation";
+                return true;
+            }
+            c.owned_extra = p;
+            S.cand = static_cast<uint64_t*>(p);
         }
         c.launch("k_join", [&] {
             if (metric == KNNG_COSINE) {

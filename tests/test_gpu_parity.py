@@ -285,3 +285,18 @@ def test_join_order_does_not_change_the_graph(K):
             assert np.array_equal(gd.cpu().numpy(), od)
     finally:
         K.knng_set_option("join_order", 0)
+
+
+def test_misaligned_rows_take_the_legacy_join(K):
+    """Rows whose base pointer is not 16-B aligned cannot use the cp.async
+    joins; the build falls back to the batched join (its staging buffer is
+    allocated on demand) and still equals the oracle."""
+    X = datagen.make("c1", 3000, seed=14, d=16)
+    oi, od = orc.build(X, 10, 8, 4, 5)
+    flat = torch.zeros(X.size + 1, dtype=torch.float32, device="cuda")
+    flat[1:] = torch.from_numpy(X.reshape(-1)).cuda()
+    Xm = flat[1:].view(3000, 16)
+    assert Xm.data_ptr() % 16 != 0
+    gi, gd = K.knng_build(Xm, 10, 4, 8, 5)
+    assert np.array_equal(gi.cpu().numpy().view(np.uint32), oi)
+    assert np.array_equal(gd.cpu().numpy(), od)
