@@ -35,7 +35,7 @@
 namespace knng {
 
 constexpr int kWsConsumerWarps = 8;
-constexpr int kWsProducerWarps = 6;  // 1 lead (batch metadata) + 5 gather warps
+constexpr int kWsProducerWarps = 8;  // 1 lead (batch metadata) + 7 gather warps
 constexpr int kWsGatherWarps = kWsProducerWarps - 1;
 constexpr int kWsEpiGroups = 2;      // epilogue groups, alternating batches
 constexpr int kWsEpiGroupWarps = 2;
