@@ -129,11 +129,6 @@ struct WsCfg {
     static_assert(kSmem <= 232448, "227 KB dynamic shared memory per CTA");
 };
 
-// Diagnostic switch (KNNG_JOIN_DBG, never set in tests or the bench):
-// 1 = consumers skip the tile arithmetic, 2 = gather warps skip the copies.
-// Isolates the data-supply and compute sides of the pipeline under ncu.
-__device__ int g_join_dbg = 0;
-
 template <typename T, bool COS, int STAGES>
 __global__ void __launch_bounds__(kWsThreads, 1)
 k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G, Samples S, int64_t boundary,
@@ -165,7 +160,6 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
     const int d = D.d, cap = D.cap;
     const int nslab = (d + SD - 1) / SD;
     const bool restricted = boundary >= 0;
-    const int dbg = g_join_dbg;
 
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -317,8 +311,7 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
                 const int e0 = sl * SD + part * CE;
                 E* dst = ring + static_cast<size_t>(st) * kWsSlots * RS;
                 const E* src0 = V + e0;
-                if (dbg == 2) {
-                } else if (sl * SD + SD <= d) {  // full slab: plain 16-B copies
+                if (sl * SD + SD <= d) {  // full slab: plain 16-B copies
                     for (int slot = row0; slot < nslots; slot += kRowsPerPass) {
                         const uint32_t id = M.ids[slot];
                         if (id == 0xFFFFFFFFu) continue;
@@ -563,7 +556,7 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
         for (int sl = 0; sl < nslab; ++sl) {
             const int st = slab_it % STAGES;
             mbar_wait(full + st, (slab_it / STAGES) & 1);
-            if (active && dbg != 1) {
+            if (active) {
                 const E* __restrict__ A = ring + static_cast<size_t>(st) * kWsSlots * RS + aoff;
                 const E* __restrict__ B = ring + static_cast<size_t>(st) * kWsSlots * RS + boff;
                 const int lim = min(SD, d - sl * SD);

@@ -352,13 +352,6 @@ struct Run {
         constexpr int NB = kJoinNodes;
         const int jk = g_opt_join_kernel.load();
         const bool force_v3 = jk == 1;
-        static const int dbg_mode = [] {
-            const char* e = getenv("KNNG_JOIN_DBG");
-            const int v = e ? atoi(e) : 0;
-            if (v) cudaMemcpyToSymbol(g_join_dbg, &v, sizeof(int));
-            return v;
-        }();
-        (void)dbg_mode;
         const bool u8_slab = al && metric == KNNG_L2SQ && dt == KNNG_U8 && D.d <= kLsRow && D.d % 16 == 0;
         if (u8_slab && (jk == 0 || jk == 5 || jk == 6)) {
             // uint8 rows of one 128-B slab: Gram tiles on the tensor cores
