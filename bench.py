@@ -293,7 +293,10 @@ def main():
 
     class Ops(CudaOps):
         """The product compute, recording each call's iteration counters."""
-        history: list = []
+
+        def __init__(self, stream=None):
+            super().__init__(stream=stream)
+            self.history = []
 
         def build(self, *a):
             r = super().build(*a)

@@ -59,7 +59,7 @@ def plan(shards: int, world: int) -> list[list[MergeStep]]:
 class CudaOps:
     """The product compute: libknng.so through the ctypes binding."""
 
-    def __init__(self, workspace=None, stream=None):
+    def __init__(self, stream=None):
         from . import knng as K
         K.lib()  # raises if the library is missing: there is no fallback
         self.K = K
