@@ -300,3 +300,17 @@ def test_misaligned_rows_take_the_legacy_join(K):
     gi, gd = K.knng_build(Xm, 10, 4, 8, 5)
     assert np.array_equal(gi.cpu().numpy().view(np.uint32), oi)
     assert np.array_equal(gd.cpu().numpy(), od)
+
+
+def test_sift_shaped_50k_end_to_end_matches_oracle(K):
+    """The bench's setting (SIFT-shaped, k = 32, p = 16, 7 iterations) at 50k
+    rows: the whole GPU graph equals the oracle's, so recall@10 on sampled
+    nodes is the oracle's (north star: within 0.005)."""
+    X = datagen.make("sift", 50000, seed=1)
+    q = datagen.sample_nodes(50000, 2000)
+    gt = orc.bruteforce(X, q, 10)
+    oi, od = orc.build(X, 32, 16, 7, 42)
+    gi, gd = K.knng_build(dev(X), 32, 7, 16, 42)
+    assert np.array_equal(gi.cpu().numpy().view(np.uint32), oi)
+    assert np.array_equal(gd.cpu().numpy(), od)
+    assert orc.recall(orc.key(od, oi)[q], gt, 10) >= 0.95
