@@ -196,8 +196,9 @@ knng_status knng_debug_philox(const uint32_t* ctr, int64_t m, uint64_t seed,
  *                  qualifies.  0: always use the float path.
  *   "join_kernel"  0 (default): automatic -- the tensor-core join
  *                  (join_tc.cuh, exact int8 Gram tiles; 8 epilogue warps, 3
- *                  CTAs per SM) for uint8 L2 rows of d <= 128, d % 16 == 0,
- *                  else the warp-specialised join (join_ws.cuh);
+ *                  CTAs per SM; rows gathered by TMA gather4) for uint8 L2
+ *                  rows of d <= 128, d % 16 == 0, else the warp-specialised
+ *                  join (join_ws.cuh);
  *                  1: the batched cp.async join (join_kernel.cuh);
  *                  2: always the warp-specialised join;
  *                  3: the lock-step ALU join (join_ls.cuh) where the
@@ -208,7 +209,9 @@ knng_status knng_debug_philox(const uint32_t* ctr, int64_t m, uint64_t seed,
  *                     a-priori error window; slower than the CUDA-core
  *                     join on B200, so opt-in;
  *                  5: the tensor-core u8 join with 4 epilogue warps, 4 CTAs
- *                     per SM; 6: 8 epilogue warps, 4 CTAs per SM.
+ *                     per SM; 6: 8 epilogue warps, 4 CTAs per SM; 7: the
+ *                     default one with 16-B cp.async row copies instead of
+ *                     TMA gather4.
  *                  All produce bit-identical graphs.
  *   "join_order"   0 (default): node-id order; 1: the uint8 tensor-core
  *                  join visits the nodes in a locality order (16-bit

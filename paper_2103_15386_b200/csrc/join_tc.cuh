@@ -40,6 +40,8 @@
 #pragma once
 #include <climits>
 
+#include <cuda.h>  // CUtensorMap (the TMA descriptor type; no driver-API linking)
+
 #include "join_ls.cuh"
 
 namespace knng {
@@ -68,7 +70,7 @@ struct TcCfg {
     static constexpr size_t kCacheCnt = 2 * 64;
     static constexpr size_t kCacheBytes = kCacheCnt + 2 * 32 * 2 * 32 * sizeof(uint32_t);
     static constexpr size_t kBarOff = (kCacheOff + kCacheBytes + 7) & ~size_t(7);
-    static constexpr size_t kCombOff = (kBarOff + 8 * (1 + 2 * kTcPlans) + 8 + 15) & ~size_t(15);
+    static constexpr size_t kCombOff = (kBarOff + 8 * (1 + 2 * kTcPlans + 2) + 8 + 15) & ~size_t(15);
     static constexpr size_t kUsed = kCombOff + 2 * kTcRows * 4;  // + upper-half partial minima (EPI = 8)
     static constexpr size_t kSmem = kUsed + 1024;  // + slack to align the rows to 1024 B
     static_assert(kTcCtasPerSm * (kSmem + 1024) <= 233472, "4 CTAs per SM");
@@ -125,14 +127,34 @@ __device__ __forceinline__ uint32_t bit_range(int a, int b) {
     return hi & ~((1u << a) - 1u);
 }
 
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+// TMA row gather: 4 rows (ids r0..r3) of the 2-D tensor map, box {128 B, 1},
+// land as 4 consecutive 128-B rows at dst (SW128 swizzle applied by the TMA
+// unit), completion counted in bytes on bar
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* tm, int r0, int r1, int r2, int r3,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+        "%4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+        "l"(tm), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // EPI epilogue warps: 4 (one thread per row), or 8 -- warps w and w + 4 read
 // the same TMEM lane quarter and split the row's column chunks, the upper
 // half handing its partial minima over through shared memory; 3 CTAs per SM
 // then keep 24 epilogue warps resident instead of 16.
-template <int EPI, int CTAS>
+// TMA: rows gathered by tcgen05-era TMA gather4 (one instruction per 4 rows,
+// issued by warp 0) instead of 16-B cp.async copies by every thread.
+template <int EPI, int CTAS, bool TMA>
 __global__ void __launch_bounds__((EPI + 1) * 32, CTAS)
 k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Graph G, Samples S, int64_t boundary,
-          unsigned long long* __restrict__ work, DevStats* __restrict__ stats, const uint32_t* __restrict__ perm) {
+          unsigned long long* __restrict__ work, DevStats* __restrict__ stats, const uint32_t* __restrict__ perm,
+          const __grid_constant__ CUtensorMap tmap) {
+    static_assert(!TMA || EPI == 8, "the TMA gather spreads 32 row groups over 8 warps x 4 lanes");
     extern __shared__ __align__(16) unsigned char tc_raw[];
     // rows need 1024-B alignment (SW128 atoms)
     unsigned char* tc_smem = tc_raw + ((1024 - (smem_u32(tc_raw) & 1023)) & 1023);
@@ -145,7 +167,8 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
     uint64_t* mma_bar = reinterpret_cast<uint64_t*>(tc_smem + TcCfg::kBarOff);
     uint64_t* plan_full = mma_bar + 1;             // [kTcPlans] planning warp -> warps 0-3
     uint64_t* plan_empty = plan_full + kTcPlans;   // [kTcPlans] warps 0-3 -> planning warp
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(plan_empty + kTcPlans);
+    uint64_t* rows_full = plan_empty + kTcPlans;  // [2] TMA row gathers of buffer 0 / 1
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rows_full + 2);
     int* comb = reinterpret_cast<int*>(tc_smem + TcCfg::kCombOff);
     constexpr int PW = EPI;  // the planning warp
 
@@ -291,7 +314,24 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
     auto gather = [&](const TcPlan& P, uint8_t* dst) {
         const int nslots = P.nslots;  // hoisted: the asm below clobbers memory
         const uint32_t dbase = smem_u32(dst);
-        if (part < nchunks) {
+        if constexpr (TMA) {
+            // group g of 4 slots is issued by lane g % 4 of warp g / 4 (the
+            // tx count may run ahead of the expect_tx: it is signed)
+            const int ng = (nslots + 3) >> 2;  // groups of 4 slots; the tail repeats a valid row
+            uint64_t* bar = rows_full + (dst == rows ? 0 : 1);
+            if (tid == 0) mbar_expect_tx(bar, static_cast<uint32_t>(ng) * 512u);
+            const int g = 4 * warp + static_cast<int>(lane);
+            if (lane < 4 && warp < EPI) {
+                if (g < ng) {
+                    const int s0 = 4 * g;
+                    const int r0 = static_cast<int>(P.ids[s0]);
+                    const int r1 = s0 + 1 < nslots ? static_cast<int>(P.ids[s0 + 1]) : r0;
+                    const int r2 = s0 + 2 < nslots ? static_cast<int>(P.ids[s0 + 2]) : r0;
+                    const int r3 = s0 + 3 < nslots ? static_cast<int>(P.ids[s0 + 3]) : r0;
+                    tma_gather4(dst + s0 * 128, &tmap, r0, r1, r2, r3, bar);
+                }
+            }
+        } else if (part < nchunks) {
             const uint8_t* src0 = X + part * 16;
             for (int slot = row0; slot < nslots; slot += EPI * 4) {
                 const uint32_t id = P.ids[slot];
@@ -300,7 +340,7 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
                              "l"(src0 + static_cast<size_t>(id) * d)
                              : "memory");
             }
-        } else if (part < kchunks) {
+        } else if (part < kchunks) {  // (cp.async path) chunks past d: zero-filled
             for (int slot = row0; slot < nslots; slot += EPI * 4)
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16, 0;\n" ::"r"(
                                  dbase + slot * 128 + ((part ^ (slot & 7)) << 4)),
@@ -358,6 +398,8 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
     }
     if (tid == 0) {
         mbar_init(mma_bar, 1);
+        mbar_init(rows_full, 1);
+        mbar_init(rows_full + 1, 1);
         for (int i = 0; i < kTcPlans; ++i) {
             mbar_init(plan_full + i, 1);
             mbar_init(plan_empty + i, PW);
@@ -410,10 +452,13 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
             const TcPlan& P = plans[slot];
             const int buf = b & 1;
             if (P.nnodes == 0) break;  // waited for at b - 2 (or in the prologue)
-            cp_async_wait<1>();        // rows(b); rows(b+1) may be in flight
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // cp.async data -> MMA operand reads
+            if constexpr (!TMA) {
+                cp_async_wait<1>();    // rows(b); rows(b+1) may be in flight
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // cp.async data -> MMA operand reads
+            }
             named_bar(1, PW * 32);  // rows(b), n'(b) visible; TMEM reads of b-1 done
             if (tid == 0) {
+                if constexpr (TMA) mbar_wait(rows_full + buf, (b >> 1) & 1);  // TMA rows(b) landed
                 tc_fence_after();
                 const uint32_t base = smem_u32(rows + buf * TcCfg::kRowBytes);
                 for (int k = 0; k < kch; ++k) {

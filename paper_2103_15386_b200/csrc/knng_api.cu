@@ -1,6 +1,7 @@
 // knng_api.cu -- the C ABI of include/knng.h: validation, workspace layout,
 // stream-ordered orchestration of the kernels, error mapping, counters.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <atomic>
 #include <cstdarg>
@@ -100,6 +101,30 @@ Layout make_layout(int64_t n, int d, int k, int p, bool cosine, bool own_keys, b
     L.flag = take(16);
     L.total = off;
     return L;
+}
+
+// 2-D TMA descriptor of uint8 rows [n][d] (d % 16 == 0, d <= 128): box of
+// one 128-B row, SW128 swizzle (the tensor-core join's shared-memory layout;
+// columns past d are zero-filled as out of bounds).  false if the driver
+// entry point is unavailable.
+bool make_row_tmap(const void* X, int64_t n, int d, CUtensorMap* tm) {
+    static PFN_cuTensorMapEncodeTiled encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        cudaGetLastError();
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+    }();
+    if (!encode) return false;
+    const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(n)};
+    const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(d)};
+    const cuuint32_t box[2] = {128, 1};
+    const cuuint32_t estride[2] = {1, 1};
+    return encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(X), gdim, gstride, box, estride,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // ---------------------------------------------------------------- context
@@ -353,7 +378,7 @@ struct Run {
         const int jk = g_opt_join_kernel.load();
         const bool force_v3 = jk == 1;
         const bool u8_slab = al && metric == KNNG_L2SQ && dt == KNNG_U8 && D.d <= kLsRow && D.d % 16 == 0;
-        if (u8_slab && (jk == 0 || jk == 5 || jk == 6)) {
+        if (u8_slab && (jk == 0 || jk == 5 || jk == 6 || jk == 7)) {
             // uint8 rows of one 128-B slab: Gram tiles on the tensor cores
             int* sqn = reinterpret_cast<int*>(ws + L.sqn);
             if (!sqn_ready) {
@@ -388,14 +413,18 @@ struct Run {
             c.launch("k_join", [&] {
                 constexpr size_t sm = TcCfg::kSmem;
                 const uint32_t* pm = perm_ready ? reinterpret_cast<const uint32_t*>(ws + L.perm) : nullptr;
+                CUtensorMap tm;
+                memset(&tm, 0, sizeof(tm));
+                const bool tma = jk == 0 && make_row_tmap(X, D.n, D.d, &tm);  // option 7: cp.async rows
                 auto go = [&](auto kfn, int ctas, int threads) {
                     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
                     kfn<<<ctas * sms, threads, sm, c.stream>>>(static_cast<const uint8_t*>(X), sqn, D, G, S, boundary,
-                                                               work, st, pm);
+                                                               work, st, pm, tm);
                 };
-                if (jk == 5) go(k_join_tc<4, 4>, 4, 5 * 32);       // 4 epilogue warps, 4 CTAs per SM
-                else if (jk == 6) go(k_join_tc<8, 4>, 4, 9 * 32);  // 8 epilogue warps, 4 CTAs per SM
-                else go(k_join_tc<8, 3>, 3, 9 * 32);               // 8 epilogue warps, 3 CTAs per SM
+                if (jk == 5) go(k_join_tc<4, 4, false>, 4, 5 * 32);       // 4 epilogue warps, 4 CTAs per SM
+                else if (jk == 6) go(k_join_tc<8, 4, false>, 4, 9 * 32);  // 8 epilogue warps, 4 CTAs per SM
+                else if (tma) go(k_join_tc<8, 3, true>, 3, 9 * 32);       // rows by TMA gather4
+                else go(k_join_tc<8, 3, false>, 3, 9 * 32);               // 8 epilogue warps, 3 CTAs per SM
             });
             return true;
         }
@@ -967,7 +996,7 @@ knng_status knng_set_option(const char* name, int64_t value) {
         return KNNG_OK;
     }
     if (strcmp(name, "join_kernel") == 0) {
-        if (value < 0 || value > 6) return fail(KNNG_E_USAGE, "join_kernel must be in [0, 6]");
+        if (value < 0 || value > 7) return fail(KNNG_E_USAGE, "join_kernel must be in [0, 7]");
         g_opt_join_kernel.store(static_cast<int>(value));
         return KNNG_OK;
     }

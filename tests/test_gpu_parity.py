@@ -201,7 +201,7 @@ def test_exact_u8_path_is_bit_identical_to_the_float_path(K):
         K.knng_set_option("exact_u8", 1)
 
 
-@pytest.mark.parametrize("jk", [0, 1, 2, 3, 5, 6])
+@pytest.mark.parametrize("jk", [0, 1, 2, 3, 5, 6, 7])
 @pytest.mark.parametrize("d", [128, 64])
 def test_join_kernels_u8_match(K, jk, d):
     """Every join kernel (auto = lock-step for these uint8 rows, legacy,
