@@ -138,6 +138,28 @@ __global__ void __launch_bounds__(256, 8) k_merge_sample(Dims D, Graph G, Sample
                 const uint32_t km = __ballot_sync(kFull, keep);
                 if (km == 0) continue;
                 const int cnt = __popc(km);
+                if (cnt <= 4) {
+                    // few survivors: insert them one by one (position by
+                    // ballot, shift by one lane) instead of a sorting network
+                    uint32_t rem = km;
+                    while (rem) {
+                        const int src = __ffs(rem) - 1;
+                        rem &= rem - 1;
+                        const uint64_t x = shfl_u64(cand, src);
+                        if (__any_sync(kFull, cur.key == x)) continue;  // repeated candidate
+                        const int pos = __popc(__ballot_sync(kFull, cur.key < x));
+                        const uint64_t up = shfl_u64(cur.key, lane > 0 ? lane - 1 : 0);
+                        const uint32_t upm = __shfl_sync(kFull, cur.meta, lane > 0 ? lane - 1 : 0);
+                        if (static_cast<int>(lane) > pos) {
+                            cur.key = up;
+                            cur.meta = upm;
+                        } else if (static_cast<int>(lane) == pos) {
+                            cur.key = x;
+                            cur.meta = 3u;  // NEW, from a bucket
+                        }
+                    }
+                    continue;
+                }
                 __syncwarp();
                 scr[lane] = kSentinel;
                 __syncwarp();
