@@ -36,6 +36,8 @@ __global__ void k_ggm_seed(const T* __restrict__ X, const float* __restrict__ Xn
     const int64_t base = own_b ? 0 : nA;
     const uint64_t size = static_cast<uint64_t>(own_b ? nA : D.n - nA);
     const uint2 key = seed_key(seed);
+    extern __shared__ uint32_t seed_scratch[];  // 32 u32 per warp
+    uint32_t* scr = seed_scratch + (threadIdx.x >> 5) * 32;
     int cnt = kh;
     for (uint32_t j0 = 0; cnt < k; j0 += 32) {
         const uint4 o = philox4x32_10(
@@ -43,21 +45,21 @@ __global__ void k_ggm_seed(const T* __restrict__ X, const float* __restrict__ Xn
         const uint32_t v = static_cast<uint32_t>(base + static_cast<int64_t>(uniform_below(o, size)));
         bool dup = false;
         for (int t = 0; t < cnt; ++t) dup |= (__shfl_sync(kFull, chosen, t) == v);
-        for (int l = 0; l < 32; ++l) {
-            const uint32_t vl = __shfl_sync(kFull, v, l);
-            dup |= (static_cast<uint32_t>(l) < lane && vl == v);
-        }
+        dup |= (__match_any_sync(kFull, v) & lanemask_lt()) != 0u;  // an earlier lane drew it
         const uint32_t acc = __ballot_sync(kFull, !dup);
-        const int want = static_cast<int>(lane) - cnt;
-        const bool take = want >= 0 && want < __popc(acc) && static_cast<int>(lane) < k;
-        const int src = take ? static_cast<int>(__fns(acc, 0, want + 1)) : 0;
-        const uint32_t got = __shfl_sync(kFull, v, src);
-        if (take) chosen = got;
-        cnt = min(k, cnt + __popc(acc));
+        // accepted draw of rank r fills lane cnt + r (compaction through shared memory)
+        __syncwarp();
+        if (!dup && cnt + __popc(acc & lanemask_lt()) < k) scr[cnt + __popc(acc & lanemask_lt())] = v;
+        __syncwarp();
+        const int nc = min(k, cnt + __popc(acc));
+        if (static_cast<int>(lane) >= cnt && static_cast<int>(lane) < nc) chosen = scr[lane];
+        cnt = nc;
     }
-    Elem e{kSentinel, 0u};
+    // (key << 1) | NEW: all k keys are distinct (kept own-subset entries and
+    // cross draws), so the flag rides in bit 0 through the sorting network
+    uint64_t e = kSentinel;
     if (static_cast<int>(lane) < kh) {
-        e = Elem{in, 0u};  // kept half: OLD
+        e = in << 1;  // kept half: OLD
     } else if (static_cast<int>(lane) < k) {
         float dist;
         if constexpr (COS) {
@@ -65,28 +67,30 @@ __global__ void k_ggm_seed(const T* __restrict__ X, const float* __restrict__ Xn
         } else {
             dist = Canon<T>::l2(X + static_cast<size_t>(i) * D.d, X + static_cast<size_t>(chosen) * D.d, D.d);
         }
-        e = Elem{make_key(dist, chosen), 1u};  // cross sample: NEW
+        e = (make_key(dist, chosen) << 1) | 1ull;  // cross sample: NEW
     }
-    e = warp_sort_elem(e);
+    e = warp_sort_u64(e);
     const bool in_list = static_cast<int>(lane) < k;
-    if (in_list) G.keys[static_cast<size_t>(i) * k + lane] = e.key;
-    const uint32_t nm = __ballot_sync(kFull, in_list && (e.meta & 1u));
+    const uint64_t ek = e == kSentinel ? kSentinel : (e >> 1);
+    if (in_list) G.keys[static_cast<size_t>(i) * k + lane] = ek;
+    const uint32_t nm = __ballot_sync(kFull, in_list && (e & 1ull));
     if (lane == 0) G.newmask[i] = nm;
-    if (static_cast<int>(lane) == k - 1) G.kth[i] = e.key;
+    if (static_cast<int>(lane) == k - 1) G.kth[i] = ek;
 }
 
 // Alg. 3 line 11: G[i] = k smallest unique keys of the refined list
 // and the reserved half G^v.
 __global__ void k_ggm_finalize(Dims D, Graph G, const uint64_t* __restrict__ reserved) {
-    extern __shared__ Elem fin_scratch[];
+    extern __shared__ uint64_t fin_scratch[];  // 32 u64 per warp
     const int64_t i = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (i >= D.n) return;
     const uint32_t lane = lane_id();
     const int k = D.k, kr = k - (k + 1) / 2;
-    Elem cur{static_cast<int>(lane) < k ? G.keys[static_cast<size_t>(i) * k + lane] : kSentinel, 0u};
+    uint64_t cur = static_cast<int>(lane) < k ? G.keys[static_cast<size_t>(i) * k + lane] : kSentinel;
+    uint32_t bits = 0;  // flags are not needed after the merge
     const uint64_t cand = static_cast<int>(lane) < kr ? reserved[static_cast<size_t>(i) * kr + lane] : kSentinel;
-    warp_merge_chunk(cur, cand, fin_scratch + (threadIdx.x >> 5) * 32);
-    if (static_cast<int>(lane) < k) G.keys[static_cast<size_t>(i) * k + lane] = cur.key;
+    warp_merge_list(cur, bits, cand, fin_scratch + (threadIdx.x >> 5) * 32);
+    if (static_cast<int>(lane) < k) G.keys[static_cast<size_t>(i) * k + lane] = cur;
 }
 
 }  // namespace knng

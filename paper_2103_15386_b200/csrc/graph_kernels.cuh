@@ -56,6 +56,8 @@ __global__ void k_init(const T* __restrict__ X, const float* __restrict__ Xn, Di
     const uint32_t lane = lane_id();
     const int k = D.k;
     const uint2 key = seed_key(seed);
+    extern __shared__ uint32_t init_scratch[];  // 32 u32 per warp
+    uint32_t* scr = init_scratch + (threadIdx.x >> 5) * 32;
     uint32_t chosen = 0xFFFFFFFFu;
     int cnt = 0;
     for (uint32_t j0 = 0; cnt < k; j0 += 32) {
@@ -66,17 +68,16 @@ __global__ void k_init(const T* __restrict__ X, const float* __restrict__ Xn, Di
         const uint32_t v = static_cast<uint32_t>(r + (r >= static_cast<uint64_t>(s) ? 1 : 0));
         bool dup = false;
         for (int t = 0; t < cnt; ++t) dup |= (__shfl_sync(kFull, chosen, t) == v);
-        for (int l = 0; l < 32; ++l) {
-            const uint32_t vl = __shfl_sync(kFull, v, l);
-            dup |= (static_cast<uint32_t>(l) < lane && vl == v);
-        }
+        dup |= (__match_any_sync(kFull, v) & lanemask_lt()) != 0u;  // an earlier lane drew it
         const uint32_t acc = __ballot_sync(kFull, !dup);
-        const int want = static_cast<int>(lane) - cnt;
-        const bool take = want >= 0 && want < __popc(acc) && static_cast<int>(lane) < k;
-        const int src = take ? static_cast<int>(__fns(acc, 0, want + 1)) : 0;
-        const uint32_t got = __shfl_sync(kFull, v, src);
-        if (take) chosen = got;
-        cnt = min(k, cnt + __popc(acc));
+        // accepted draw of rank r fills lane cnt + r (compaction through shared memory)
+        const int slot = cnt + __popc(acc & lanemask_lt());
+        __syncwarp();
+        if (!dup && slot < k) scr[slot] = v;
+        __syncwarp();
+        const int nc = min(k, cnt + __popc(acc));
+        if (static_cast<int>(lane) >= cnt && static_cast<int>(lane) < nc) chosen = scr[lane];
+        cnt = nc;
     }
     uint64_t kk = kSentinel;
     if (static_cast<int>(lane) < k) {

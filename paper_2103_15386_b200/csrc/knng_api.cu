@@ -327,11 +327,11 @@ struct Run {
         const int grid = warps_grid(D.n, wpb);
         c.launch("k_init", [&] {
             if (metric == KNNG_COSINE)
-                k_init<float, true><<<grid, wpb * 32, 0, c.stream>>>(nullptr, Xn, D, seed, G);
+                k_init<float, true><<<grid, wpb * 32, wpb * 32 * 4, c.stream>>>(nullptr, Xn, D, seed, G);
             else if (dt == KNNG_F32)
-                k_init<float, false><<<grid, wpb * 32, 0, c.stream>>>(static_cast<const float*>(X), nullptr, D, seed, G);
+                k_init<float, false><<<grid, wpb * 32, wpb * 32 * 4, c.stream>>>(static_cast<const float*>(X), nullptr, D, seed, G);
             else
-                k_init<uint8_t, false><<<grid, wpb * 32, 0, c.stream>>>(static_cast<const uint8_t*>(X), nullptr, D, seed, G);
+                k_init<uint8_t, false><<<grid, wpb * 32, wpb * 32 * 4, c.stream>>>(static_cast<const uint8_t*>(X), nullptr, D, seed, G);
         });
     }
 
@@ -920,13 +920,13 @@ knng_status knng_merge(const void* vecA, int64_t nA, const uint32_t* idsA, const
     const int grid = R.warps_grid(n, 8);
     c.launch("k_ggm_seed", [&] {
         if (metric == KNNG_COSINE)
-            k_ggm_seed<float, true><<<grid, 256, 0, c.stream>>>(nullptr, R.Xn, R.D, nA, level, seed, idsA, distsA, idsB,
+            k_ggm_seed<float, true><<<grid, 256, 256 * 4, c.stream>>>(nullptr, R.Xn, R.D, nA, level, seed, idsA, distsA, idsB,
                                                                 distsB, R.G, reserved);
         else if (R.dt == KNNG_F32)
-            k_ggm_seed<float, false><<<grid, 256, 0, c.stream>>>(reinterpret_cast<const float*>(R.X), nullptr, R.D, nA,
+            k_ggm_seed<float, false><<<grid, 256, 256 * 4, c.stream>>>(reinterpret_cast<const float*>(R.X), nullptr, R.D, nA,
                                                                  level, seed, idsA, distsA, idsB, distsB, R.G, reserved);
         else
-            k_ggm_seed<uint8_t, false><<<grid, 256, 0, c.stream>>>(reinterpret_cast<const uint8_t*>(R.X), nullptr, R.D,
+            k_ggm_seed<uint8_t, false><<<grid, 256, 256 * 4, c.stream>>>(reinterpret_cast<const uint8_t*>(R.X), nullptr, R.D,
                                                                    nA, level, seed, idsA, distsA, idsB, distsB, R.G,
                                                                    reserved);
     });
@@ -934,7 +934,7 @@ knng_status knng_merge(const void* vecA, int64_t nA, const uint32_t* idsA, const
         R.iteration(t, 0x80000000u | (static_cast<uint32_t>(level) << 16) | static_cast<uint32_t>(t), t > 0);
     R.merge_sample(1, 0, merge_iters - 1);
     c.launch("k_ggm_finalize", [&] {
-        k_ggm_finalize<<<grid, 256, 256 / 32 * 32 * sizeof(Elem), c.stream>>>(R.D, R.G, reserved);
+        k_ggm_finalize<<<grid, 256, 256 * sizeof(uint64_t), c.stream>>>(R.D, R.G, reserved);
     });
     R.export_graph(out_ids, out_dists);
     R.collect_stats(merge_iters);
