@@ -59,10 +59,12 @@ def main():
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--shards", type=int, default=8)
     ap.add_argument("--iters", default="7", help="comma list: every value is measured")
-    ap.add_argument("--merge-iters", type=int, default=6)
+    ap.add_argument("--merge-iters", default="6", help="one count, or one per tree level (comma list)")
     ap.add_argument("--p", type=int, default=None, help="sample size (default: 16 for c3/c4, 8 for c5)")
     ap.add_argument("--no-tree", action="store_true")
     a = ap.parse_args()
+    mi = [int(x) for x in str(a.merge_iters).split(",")]
+    a.merge_iters = mi[0] if len(mi) == 1 else mi
     out = []
     if a.config == "c3":
         n = a.n or 1_000_000
