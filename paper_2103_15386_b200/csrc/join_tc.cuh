@@ -515,8 +515,6 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
             const int cs = upper ? c0 + 16 * half : c0;
             const int ce = upper ? whi : min(whi, c0 + 16 * half);
             for (int cb = cs; cb < ce; cb += 16) {
-                uint32_t r[16];
-                tc_ld16(tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + cb, r);
                 uint32_t A = act ? bit_range(sb - cb, sb + m - cb) : 0u;
                 if (isNEW && s >= cb && s < cb + 16) A &= ~(1u << (s - cb));
                 uint32_t B = isNEW ? bit_range(sb + m - cb, sb + m + q - cb) : 0u;
@@ -525,7 +523,12 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
                     const uint32_t allow = myside ? ~sd : sd;
                     A &= allow;
                     B &= allow;
+                    // a GGM refine leaves whole chunks without a cross pair
+                    // (NEW x NEW is always same-subset, D22): skip their loads
+                    if (!__any_sync(kFull, ((A | B) & 0xFFFFu) != 0u)) continue;
                 }
+                uint32_t r[16];
+                tc_ld16(tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + cb, r);
                 A &= 0xFFFFu;
                 B &= 0xFFFFu;
                 if (isNEW) my_pairs += __popc(A & bit_range(0, s - cb)) + __popc(B);
