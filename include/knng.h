@@ -211,7 +211,9 @@ knng_status knng_debug_philox(const uint32_t* ctr, int64_t m, uint64_t seed,
  *                  5: the tensor-core u8 join with 4 epilogue warps, 4 CTAs
  *                     per SM; 6: 8 epilogue warps, 4 CTAs per SM; 7: the
  *                     default one with 16-B cp.async row copies instead of
- *                     TMA gather4.
+ *                     TMA gather4; 8: float rows (d % 4 == 0) staged into the
+ *                     warp-specialised join by TMA gather4 (no faster on
+ *                     B200).
  *                  All produce bit-identical graphs.
  *   "join_order"   0 (default): node-id order; 1: the uint8 tensor-core
  *                  join visits the nodes in a locality order (16-bit

@@ -40,7 +40,6 @@
 #pragma once
 #include <climits>
 
-#include <cuda.h>  // CUtensorMap (the TMA descriptor type; no driver-API linking)
 
 #include "join_ls.cuh"
 
@@ -125,22 +124,6 @@ __device__ __forceinline__ uint32_t bit_range(int a, int b) {
     if (a >= b) return 0u;
     const uint32_t hi = b >= 32 ? 0xFFFFFFFFu : ((1u << b) - 1u);
     return hi & ~((1u << a) - 1u);
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-// TMA row gather: 4 rows (ids r0..r3) of the 2-D tensor map, box {128 B, 1},
-// land as 4 consecutive 128-B rows at dst (SW128 swizzle applied by the TMA
-// unit), completion counted in bytes on bar
-__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* tm, int r0, int r1, int r2, int r3,
-                                            uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
-        "%4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
-        "l"(tm), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
-        : "memory");
 }
 
 // EPI epilogue warps: 4 (one thread per row), or 8 -- warps w and w + 4 read

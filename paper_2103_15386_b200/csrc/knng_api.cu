@@ -107,7 +107,7 @@ Layout make_layout(int64_t n, int d, int k, int p, bool cosine, bool own_keys, b
 // one 128-B row, SW128 swizzle (the tensor-core join's shared-memory layout;
 // columns past d are zero-filled as out of bounds).  false if the driver
 // entry point is unavailable.
-bool make_row_tmap(const void* X, int64_t n, int d, CUtensorMap* tm) {
+PFN_cuTensorMapEncodeTiled tmap_encoder() {
     static PFN_cuTensorMapEncodeTiled encode = [] {
         void* fn = nullptr;
         cudaDriverEntryPointQueryResult q;
@@ -117,12 +117,31 @@ bool make_row_tmap(const void* X, int64_t n, int d, CUtensorMap* tm) {
         cudaGetLastError();
         return reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
     }();
+    return encode;
+}
+bool make_row_tmap(const void* X, int64_t n, int d, CUtensorMap* tm) {
+    PFN_cuTensorMapEncodeTiled encode = tmap_encoder();
     if (!encode) return false;
     const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(n)};
     const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(d)};
     const cuuint32_t box[2] = {128, 1};
     const cuuint32_t estride[2] = {1, 1};
     return encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(X), gdim, gstride, box, estride,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// 2-D TMA descriptor of float rows [n][d] (d % 4 == 0): box of one 128-B
+// slab (32 floats) of one row, SW128 swizzle (the float join's ring layout);
+// columns past d are zero-filled as out of bounds.
+bool make_f32_slab_tmap(const float* X, int64_t n, int d, CUtensorMap* tm) {
+    PFN_cuTensorMapEncodeTiled encode = tmap_encoder();
+    if (!encode) return false;
+    const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(n)};
+    const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(d) * 4};
+    const cuuint32_t box[2] = {32, 1};
+    const cuuint32_t estride[2] = {1, 1};
+    return encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(X), gdim, gstride, box, estride,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -480,21 +499,45 @@ struct Run {
             constexpr int STG = 5;
             unsigned long long* work = reinterpret_cast<unsigned long long*>(ws + L.flag + 8);
             cudaMemsetAsync(work, 0, 8, c.stream);
+            // float rows: 16-B cp.async copies by the gather warps; option
+            // join_kernel 8 stages them by TMA gather4 instead (bit-identical;
+            // measured no faster: DEEP-shaped 10.8 vs 10.9 ms, GIST-shaped
+            // 14.1 vs 12.4 ms per launch -- the consumers, not the copies,
+            // bound this kernel; profiles/r01s2_join_ws_tma.txt)
+            CUtensorMap tm;
+            memset(&tm, 0, sizeof(tm));
+            const float* Xf = metric == KNNG_COSINE ? Xn : static_cast<const float*>(X);
+            const bool tma = (metric == KNNG_COSINE || dt == KNNG_F32) && jk == 8 && D.d % 4 == 0 &&
+                             make_f32_slab_tmap(Xf, D.n, D.d, &tm);
             c.launch("k_join", [&] {
                 if (metric == KNNG_COSINE) {
                     constexpr size_t sm = WsCfg<float, true, STG>::kSmem;
-                    cudaFuncSetAttribute(k_join_ws<float, true, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-                    k_join_ws<float, true, STG><<<sms, kWsThreads, sm, c.stream>>>(nullptr, Xn, D, G, S, boundary, work, st);
+                    if (tma) {
+                        cudaFuncSetAttribute(k_join_ws<float, true, STG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(sm + 1024));
+                        k_join_ws<float, true, STG, true><<<sms, kWsThreads, sm + 1024, c.stream>>>(nullptr, Xn, D, G, S,
+                                                                                                    boundary, work, st, tm);
+                    } else {
+                        cudaFuncSetAttribute(k_join_ws<float, true, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+                        k_join_ws<float, true, STG><<<sms, kWsThreads, sm, c.stream>>>(nullptr, Xn, D, G, S, boundary, work, st, tm);
+                    }
                 } else if (dt == KNNG_F32) {
                     constexpr size_t sm = WsCfg<float, false, STG>::kSmem;
-                    cudaFuncSetAttribute(k_join_ws<float, false, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-                    k_join_ws<float, false, STG><<<sms, kWsThreads, sm, c.stream>>>(static_cast<const float*>(X), nullptr, D,
-                                                                                    G, S, boundary, work, st);
+                    if (tma) {
+                        cudaFuncSetAttribute(k_join_ws<float, false, STG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(sm + 1024));
+                        k_join_ws<float, false, STG, true><<<sms, kWsThreads, sm + 1024, c.stream>>>(
+                            static_cast<const float*>(X), nullptr, D, G, S, boundary, work, st, tm);
+                    } else {
+                        cudaFuncSetAttribute(k_join_ws<float, false, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+                        k_join_ws<float, false, STG><<<sms, kWsThreads, sm, c.stream>>>(static_cast<const float*>(X), nullptr,
+                                                                                        D, G, S, boundary, work, st, tm);
+                    }
                 } else {
                     constexpr size_t sm = WsCfg<uint8_t, false, STG>::kSmem;
                     cudaFuncSetAttribute(k_join_ws<uint8_t, false, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
                     k_join_ws<uint8_t, false, STG><<<sms, kWsThreads, sm, c.stream>>>(static_cast<const uint8_t*>(X), nullptr,
-                                                                                      D, G, S, boundary, work, st);
+                                                                                      D, G, S, boundary, work, st, tm);
                 }
             });
             return true;
@@ -996,7 +1039,7 @@ knng_status knng_set_option(const char* name, int64_t value) {
         return KNNG_OK;
     }
     if (strcmp(name, "join_kernel") == 0) {
-        if (value < 0 || value > 7) return fail(KNNG_E_USAGE, "join_kernel must be in [0, 7]");
+        if (value < 0 || value > 8) return fail(KNNG_E_USAGE, "join_kernel must be in [0, 8]");
         g_opt_join_kernel.store(static_cast<int>(value));
         return KNNG_OK;
     }
