@@ -165,6 +165,7 @@ k_join_ls(const uint8_t* __restrict__ X, Dims D, Graph G, Samples S, int64_t bou
             if (!more || !advance()) {
                 more = false;
                 if (lane == 0) P.nnodes = 0;
+                __syncwarp();  // the terminator is read by every lane
                 return;
             }
         }

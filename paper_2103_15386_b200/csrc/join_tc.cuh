@@ -248,6 +248,7 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
             if (!more || !advance()) {
                 more = false;
                 if (lane == 0) P.nnodes = 0;
+                __syncwarp();  // the terminator is read by every lane
                 return;
             }
         }

@@ -195,6 +195,7 @@ k_join_tcf(const float* __restrict__ X, const float* __restrict__ sqn, Dims D, G
             if (!more || !advance()) {
                 more = false;
                 if (lane == 0) P.nnodes = 0;
+                __syncwarp();  // the terminator is read by every lane
                 return;
             }
         }

@@ -288,6 +288,11 @@ struct Run {
         if (c.err != cudaSuccess) return false;
         cudaMemsetAsync(G.bcnt, 0, static_cast<size_t>(D.n) * 4, c.stream);
         cudaMemsetAsync(S.rcnt, 0, static_cast<size_t>(2) * D.n * 4, c.stream);
+        // k_rev_select loads whole forward rows ahead of their counts (the
+        // entries past the count are discarded): keep them initialised
+        cudaMemsetAsync(S.fwd, 0xFF, static_cast<size_t>(2) * D.n * D.p * 4, c.stream);
+        // likewise the joins' planning warps copy whole sample rows (cap ids)
+        cudaMemsetAsync(S.G, 0xFF, static_cast<size_t>(2) * D.n * D.cap * 4, c.stream);
         cudaMemsetAsync(stats, 0, sizeof(DevStats) * kMaxIters, c.stream);
         return true;
     }
