@@ -176,16 +176,33 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def recall_at_10(K, Xd, dists, nodes):
-    """recall@10 on `nodes` sampled nodes against the exact k-NN
+def recall_at_10(K, Xd, dists, nodes, ids=None):
+    """recall@10 (Eq. 4) on `nodes` sampled nodes against the exact k-NN
     (knng_bruteforce), with the D27 tie rule: entry j of the first 10 counts
-    iff d(i, j) <= d_true,10(i)."""
+    iff d(i, j) <= d_true,10(i).  When the ids are given, the graph is first
+    checked independently of its own reported distances: on the sampled rows
+    every id is a valid non-self node, no id repeats, and every stored
+    distance equals the distance recomputed in float64 from the two vectors
+    (within 1e-5 relative, BASELINE.json north_star); the tie rule then uses
+    the verified distances."""
     import torch
 
     import datagen
     q = datagen.sample_nodes(Xd.shape[0], nodes)
+    qt = torch.from_numpy(q).cuda().long()
     _, gd = K.knng_bruteforce(Xd, torch.from_numpy(q), 10)
-    mine = dists[torch.from_numpy(q).cuda().long(), :10]
+    mine = dists[qt, :10]
+    if ids is not None:
+        gi = ids[qt].long()
+        assert (gi >= 0).all() and (gi < Xd.shape[0]).all(), "graph id out of range"
+        assert (gi != qt[:, None]).all(), "self-loop in the graph"
+        srt = gi.sort(dim=1).values
+        assert (srt[:, 1:] != srt[:, :-1]).all(), "duplicate id in a list"
+        x = Xd[qt].double()
+        for j in range(gi.shape[1]):
+            ref = ((Xd[gi[:, j]].double() - x) ** 2).sum(1)
+            got = dists[qt, j].double()
+            assert ((got - ref).abs() <= 1e-5 * ref.abs().clamp_min(1e-30)).all(), "stored distance != recomputed"
     return float((mine <= gd[:, 9:10]).float().mean().item()), len(q)
 
 
@@ -358,7 +375,7 @@ def main():
         recall, nq = recall_at_10(K, Xall, Dall, args.recall_nodes) if rank == 0 else (None, 0)
         del Xall, Dall
     else:
-        recall, nq = recall_at_10(K, Xd, dists, args.recall_nodes)
+        recall, nq = recall_at_10(K, Xd, dists, args.recall_nodes, ids)
 
     # ---- end to end through the public API (pinned host buffers, copies timed)
     e2e = None

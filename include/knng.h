@@ -81,7 +81,8 @@ typedef struct {
  *   seed       key of every Philox draw (D31)
  *   out_ids    [n][k] device u32;  out_dists [n][k] device f32
  *   workspace  device scratch of >= knng_build_workspace_bytes(...) bytes,
- *              or NULL with workspace_bytes == 0 to let the library allocate
+ *              256-byte aligned (else KNNG_E_USAGE), or NULL with
+ *              workspace_bytes == 0 to let the library allocate
  *              (cudaMallocAsync on `stream`) and free it before returning.
  * ---------------------------------------------------------------------- */
 size_t knng_build_workspace_bytes(knng_dtype dt, int64_t n, int32_t d,
@@ -198,31 +199,15 @@ knng_status knng_debug_philox(const uint32_t* ctr, int64_t m, uint64_t seed,
  *                  (join_tc.cuh, exact int8 Gram tiles; 8 epilogue warps, 3
  *                  CTAs per SM; rows gathered by TMA gather4) for uint8 L2
  *                  rows of d <= 128, d % 16 == 0, else the warp-specialised
- *                  join (join_ws.cuh);
- *                  1: the batched cp.async join (join_kernel.cuh);
+ *                  CUDA-core join (join_ws.cuh);
+ *                  1: the batched cp.async join (join_kernel.cuh; also the
+ *                     automatic choice for rows that are not 16-B aligned);
  *                  2: always the warp-specialised join;
- *                  3: the lock-step ALU join (join_ls.cuh) where the
- *                     tensor-core join would run;
  *                  4: float rows (L2 / cosine, d % 4 == 0, d <= 128): the
  *                     TF32 tensor-core join (join_tcf.cuh) -- exact
  *                     selection by canonical recomputation inside an
- *                     a-priori error window; slower than the CUDA-core
- *                     join on B200, so opt-in;
- *                  5: the tensor-core u8 join with 4 epilogue warps, 4 CTAs
- *                     per SM; 6: 8 epilogue warps, 4 CTAs per SM; 7: the
- *                     default one with 16-B cp.async row copies instead of
- *                     TMA gather4; 8: float rows (d % 4 == 0) staged into the
- *                     warp-specialised join by TMA gather4 (no faster on
- *                     B200).
+ *                     a-priori error window.
  *                  All produce bit-identical graphs.
- *   "join_order"   0 (default): node-id order; 1: the uint8 tensor-core
- *                  join visits the nodes in a locality order (16-bit
- *                  random-projection code, counting sort; order_kernels.cuh)
- *                  so that nodes with overlapping sample sets run together.
- *                  The result does not depend on it (bulk-synchronous
- *                  update, D17).  Measured on C2: 2.66 -> 2.58 ms per join
- *                  launch for ~1 ms of ordering per build -- no net gain,
- *                  hence off.
  *   "last_exact_u8" (read-only) 1 if the last build/merge on this thread ran
  *                  on the exact integer path.
  * ---------------------------------------------------------------------- */

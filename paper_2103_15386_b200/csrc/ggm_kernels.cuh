@@ -14,7 +14,7 @@ template <typename T, bool COS>
 __global__ void k_ggm_seed(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, int64_t nA, int level,
                            uint64_t seed, const uint32_t* __restrict__ idsA, const float* __restrict__ distsA,
                            const uint32_t* __restrict__ idsB, const float* __restrict__ distsB, Graph G,
-                           uint64_t* __restrict__ reserved) {
+                           uint64_t* __restrict__ reserved, int* __restrict__ bad) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (i >= D.n) return;
     const uint32_t lane = lane_id();
@@ -22,11 +22,16 @@ __global__ void k_ggm_seed(const T* __restrict__ X, const float* __restrict__ Xn
     const bool own_b = i >= nA;
     uint64_t in = kSentinel;
     if (static_cast<int>(lane) < k) {
+        // input ids must lie in their own graph's range (else KNNG_E_USAGE)
         if (!own_b) {
-            in = make_key(distsA[static_cast<size_t>(i) * k + lane], idsA[static_cast<size_t>(i) * k + lane]);
+            const uint32_t id = idsA[static_cast<size_t>(i) * k + lane];
+            if (id >= static_cast<uint64_t>(nA)) atomicExch(bad, 1);
+            in = make_key(distsA[static_cast<size_t>(i) * k + lane], id);
         } else {
             const size_t o = static_cast<size_t>(i - nA) * k + lane;
-            in = make_key(distsB[o], static_cast<uint32_t>(idsB[o] + nA));
+            const uint32_t id = idsB[o];
+            if (id >= static_cast<uint64_t>(D.n - nA)) atomicExch(bad, 1);
+            in = make_key(distsB[o], static_cast<uint32_t>(id + nA));
         }
     }
     if (static_cast<int>(lane) >= kh && static_cast<int>(lane) < k)

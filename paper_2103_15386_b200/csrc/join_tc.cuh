@@ -41,11 +41,12 @@
 #include <climits>
 
 
-#include "join_ls.cuh"
+#include "join_ws.cuh"
 
 namespace knng {
 
 constexpr int kTcRows = 128;     // sample slots per batch = MMA M = N
+constexpr int kTcRowBytes = 128;  // bytes per staged row (uint8 rows of d <= 128)
 constexpr int kTcWarps = 5;      // 4 epilogue/gather + 1 planning
 constexpr int kTcThreads = kTcWarps * 32;
 constexpr int kTcPlanWarp = 4;
@@ -135,7 +136,7 @@ __device__ __forceinline__ uint32_t bit_range(int a, int b) {
 template <int EPI, int CTAS, bool TMA>
 __global__ void __launch_bounds__((EPI + 1) * 32, CTAS)
 k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Graph G, Samples S, int64_t boundary,
-          unsigned long long* __restrict__ work, DevStats* __restrict__ stats, const uint32_t* __restrict__ perm,
+          unsigned long long* __restrict__ work, DevStats* __restrict__ stats,
           const __grid_constant__ CUtensorMap tmap) {
     static_assert(!TMA || EPI == 8, "the TMA gather spreads 32 row groups over 8 warps x 4 lanes");
     extern __shared__ __align__(16) unsigned char tc_raw[];
@@ -179,18 +180,8 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
     auto fetch = [&](int buf, int64_t xb) {
         if (xb < D.n) {
             const int nodes = static_cast<int>(D.n - xb < 32 ? D.n - xb : 32);
-            // node of chunk slot `lane`: xb + lane, or perm[xb + lane] (the
-            // locality order of order_kernels.cuh; needs cap % 4 == 0)
-            int64_t xl = xb + lane;
-            if (perm) {
-                uint32_t c2 = 0;
-                if (static_cast<int>(lane) < nodes) {
-                    xl = perm[xb + lane];
-                    c2 = *reinterpret_cast<const uint16_t*>(S.gcnt + 2 * xl);
-                }
-                cc_cnt[buf * 64 + 2 * lane] = static_cast<uint8_t>(c2);
-                cc_cnt[buf * 64 + 2 * lane + 1] = static_cast<uint8_t>(c2 >> 8);
-            } else if (lane < 16) {
+            const int64_t xl = xb + lane;
+            if (lane < 16) {
                 const int lo = 4 * static_cast<int>(lane), bytes = max(0, min(4, 2 * nodes - lo));
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(smem_u32(cc_cnt + buf * 64 + lo)),
                              "l"(S.gcnt + 2 * xb + lo), "r"(bytes)

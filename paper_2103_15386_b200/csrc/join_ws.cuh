@@ -149,21 +149,10 @@ struct WsCfg {
     static_assert(kSmem + 1024 <= 232448, "227 KB dynamic shared memory per CTA (+ 1 KB TMA alignment)");
 };
 
-// Physical ring slot of logical slot i when the rows are staged by TMA:
-// the 4 rows of a consumer block (4-aligned logical slots) go 8 slots apart,
-// so the SW128 swizzle the TMA unit applies (chunk ^ (slot & 7)) equals the
-// (logical slot >> 2) & 7 swizzle the blocks are conflict-free with.
-__device__ __forceinline__ int ws_phys(int i) { return (i & ~31) | ((i & 3) << 3) | ((i >> 2) & 7); }
-__device__ __forceinline__ int ws_logical(int p) { return (p & ~31) | ((p & 7) << 2) | ((p >> 3) & 3); }
-
-// TMA: float rows staged by TMA gather4 (4 rows x one 128-B slab per
-// instruction) into the permuted, SW128-swizzled ring instead of 16-B
-// cp.async copies by the gather warps.
-template <typename T, bool COS, int STAGES, bool TMA = false>
+template <typename T, bool COS, int STAGES>
 __global__ void __launch_bounds__(kWsThreads, 1)
 k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G, Samples S, int64_t boundary,
-          unsigned long long* __restrict__ work, DevStats* __restrict__ stats,
-          const __grid_constant__ CUtensorMap tmap) {
+          unsigned long long* __restrict__ work, DevStats* __restrict__ stats) {
     using Cfg = WsCfg<T, COS, STAGES>;
     using E = typename Cfg::E;
     constexpr bool kFloat = std::is_same<E, float>::value;
@@ -172,8 +161,7 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
     const E* __restrict__ V = COS ? reinterpret_cast<const E*>(Xn) : reinterpret_cast<const E*>(X);
 
     extern __shared__ __align__(128) unsigned char ws_raw[];
-    // the TMA's SW128 pattern is anchored to 1024-B address boundaries
-    unsigned char* ws_smem = TMA ? ws_raw + ((1024 - (smem_u32(ws_raw) & 1023)) & 1023) : ws_raw;
+    unsigned char* ws_smem = ws_raw;
     E* ring = reinterpret_cast<E*>(ws_smem);
     WsMeta* meta = reinterpret_cast<WsMeta*>(ws_smem + Cfg::kMetaOff);
     unsigned long long* parts = reinterpret_cast<unsigned long long*>(ws_smem + Cfg::kPartOff);  // [2][8][blocks]
@@ -196,7 +184,7 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
 
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(full + s, TMA ? 1 : kWsProdThreads);  // expect_tx once / one cp.async arrive per gather thread
+            mbar_init(full + s, kWsProdThreads);  // one cp.async arrive per gather thread
             mbar_init(empty + s, kWsConsumerWarps);
         }
         for (int s = 0; s < kWsMeta; ++s) {
@@ -338,29 +326,6 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
         const int row0 = ptid / CPR;
         auto gather = [&](const WsMeta& M) {
             const int nslots = M.nslots;
-            if constexpr (TMA) {
-                // one gather4 per 4 physical slots: whole 32-slot blocks that
-                // hold logical slots < nslots; padding slots load row ids[0]
-                const int ngroups = ((nslots + 31) >> 5) * 8;
-                const uint32_t dummy = M.ids[0];
-                for (int sl = 0; sl < nslab; ++sl) {
-                    const int st = slab_it % STAGES;
-                    mbar_wait_sleep(empty + st, ((slab_it / STAGES) & 1) ^ 1);
-                    E* dst = ring + static_cast<size_t>(st) * kWsSlots * RS;
-                    if (ptid == 0) mbar_expect_tx(full + st, static_cast<uint32_t>(ngroups) * 512u);
-                    for (int g = ptid; g < ngroups; g += kWsProdThreads) {
-                        int r[4];
-#pragma unroll
-                        for (int t = 0; t < 4; ++t) {
-                            const int li = ws_logical(4 * g + t);
-                            const uint32_t id = li < nslots ? M.ids[li] : 0xFFFFFFFFu;
-                            r[t] = static_cast<int>(id == 0xFFFFFFFFu ? dummy : id);
-                        }
-                        tma_gather4(dst + 4 * g * RS, &tmap, r[0], r[1], r[2], r[3], full + st, sl * SD);
-                    }
-                    ++slab_it;
-                }
-            } else {
             for (int sl = 0; sl < nslab; ++sl) {
                 const int st = slab_it % STAGES;
                 mbar_wait_sleep(empty + st, ((slab_it / STAGES) & 1) ^ 1);
@@ -388,7 +353,6 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
                 asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full + st))
                              : "memory");
                 ++slab_it;
-            }
             }
         };
         if (warp < kWsConsumerWarps + kWsGatherWarps) {  // gather warps follow the batch stream
@@ -601,8 +565,8 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
         const bool nn_blk = J < mg;
         const int rb = 4 * I;
         const int cb = nn_blk ? 4 * J : mpad + 4 * (J - mg);
-        const int aoff = (TMA ? ws_phys(sb + rb) : sb + rb) * RS, boff = (TMA ? ws_phys(sb + cb) : sb + cb) * RS;
-        constexpr int RW = TMA ? 8 * RS : RS;  // ring distance between a block's rows
+        const int aoff = (sb + rb) * RS, boff = (sb + cb) * RS;
+        constexpr int RW = RS;  // ring distance between a block's rows
         const int fA = ((sb + rb) >> 2) & 7, fB = ((sb + cb) >> 2) & 7;  // chunk swizzle
 
         Acc acc[4][4];

@@ -16,10 +16,8 @@
 #include "eval_kernels.cuh"
 #include "ggm_kernels.cuh"
 #include "join_kernel.cuh"
-#include "join_ls.cuh"
 #include "join_tc.cuh"
 #include "join_tcf.cuh"
-#include "order_kernels.cuh"
 #include "join_ws.cuh"
 
 using namespace knng;
@@ -32,7 +30,6 @@ std::atomic<int64_t> g_launches{0};
 std::atomic<int> g_timing{0};
 std::atomic<int> g_opt_exact_u8{1};
 std::atomic<int> g_opt_join_kernel{0};
-std::atomic<int> g_opt_join_order{0};
 thread_local int g_last_exact_u8 = 0;
 std::mutex g_time_mu;
 std::map<std::string, std::pair<double, int64_t>> g_times;
@@ -51,7 +48,7 @@ constexpr int kMaxIters = 256;
 
 // ---------------------------------------------------------------- layout
 struct Layout {
-    size_t keys, newmask, kth, bcnt, bucket, fwd, fcnt, rcnt, fpos, off, osum, ocode, ohist, perm, rsrc, G, gcnt, bsum, cand, stats,
+    size_t keys, newmask, kth, bcnt, bucket, fwd, fcnt, rcnt, fpos, off, rsrc, G, gcnt, bsum, cand, stats,
         xnorm, xu8, sqn, reserved, flag, total;
     bool has_cand;
 };
@@ -94,10 +91,6 @@ Layout make_layout(int64_t n, int d, int k, int p, bool cosine, bool own_keys, b
     L.reserved = merge ? take(static_cast<size_t>(n) * (k / 2 > 0 ? k / 2 : 1) * 8) : 0;
     L.xu8 = u8copy ? take(static_cast<size_t>(n) * d) : 0;  // exact integer copy (option exact_u8)
     L.sqn = take(static_cast<size_t>(n) * 4);                // exact squared norms (uint8 tensor-core join)
-    L.osum = take(static_cast<size_t>(d) * 4);               // join order: column sums,
-    L.ocode = take(static_cast<size_t>(n) * 4);              //   projection codes,
-    L.ohist = take(static_cast<size_t>(kOrderBuckets) * 4);  //   bucket offsets,
-    L.perm = take(static_cast<size_t>(n) * 4);               //   node order
     L.flag = take(16);
     L.total = off;
     return L;
@@ -134,7 +127,7 @@ bool make_row_tmap(const void* X, int64_t n, int d, CUtensorMap* tm) {
 // 2-D TMA descriptor of float rows [n][d] (d % 4 == 0): box of one 128-B
 // slab (32 floats) of one row, SW128 swizzle (the float join's ring layout);
 // columns past d are zero-filled as out of bounds.
-bool make_f32_slab_tmap(const float* X, int64_t n, int d, CUtensorMap* tm) {
+[[maybe_unused]] bool make_f32_slab_tmap(const float* X, int64_t n, int d, CUtensorMap* tm) {
     PFN_cuTensorMapEncodeTiled encode = tmap_encoder();
     if (!encode) return false;
     const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(n)};
@@ -254,9 +247,15 @@ struct Run {
     uint64_t seed;
     int64_t boundary = -1;
     bool sqn_ready = false;   // L.sqn holds the exact squared norms of X
-    bool perm_ready = false;  // L.perm holds the join order
+    int sms = 148;            // SM count of the current device (persistent grids)
 
-    Run(Ctx& ctx) : c(ctx) {}
+    Run(Ctx& ctx) : c(ctx) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms < 1)
+            sms = 148;
+        cudaGetLastError();
+    }
 
     void bind(char* base, uint64_t* keys) {
         ws = base;
@@ -332,14 +331,14 @@ struct Run {
         const int64_t total = D.n * D.d;
         cudaMemsetAsync(flag, 0, 4, c.stream);
         c.launch("k_check_u8", [&] {
-            k_check_u8<<<4 * 148, 256, 0, c.stream>>>(static_cast<const float*>(X), total, flag);
+            k_check_u8<<<4 * sms, 256, 0, c.stream>>>(static_cast<const float*>(X), total, flag);
         });
         int h = 1;
         cudaMemcpyAsync(&h, flag, 4, cudaMemcpyDeviceToHost, c.stream);
         if (cudaStreamSynchronize(c.stream) != cudaSuccess || h) return;
         uint8_t* xu8 = reinterpret_cast<uint8_t*>(ws + L.xu8);
         c.launch("k_to_u8", [&] {
-            k_to_u8<<<4 * 148, 256, 0, c.stream>>>(static_cast<const float*>(X), total, xu8);
+            k_to_u8<<<4 * sms, 256, 0, c.stream>>>(static_cast<const float*>(X), total, xu8);
         });
         X = xu8;
         dt = KNNG_U8;
@@ -390,8 +389,6 @@ struct Run {
 
     // returns true when the candidates were filed inside the join kernel
     bool join(int iter) {
-        int sms = 148;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
         const int64_t batches = (D.n + kJoinNodes - 1) / kJoinNodes;
         const int grid = static_cast<int>(batches < 8ll * sms ? batches : 8ll * sms);
         DevStats* st = stats + iter;
@@ -401,8 +398,8 @@ struct Run {
         constexpr int NB = kJoinNodes;
         const int jk = g_opt_join_kernel.load();
         const bool force_v3 = jk == 1;
-        const bool u8_slab = al && metric == KNNG_L2SQ && dt == KNNG_U8 && D.d <= kLsRow && D.d % 16 == 0;
-        if (u8_slab && (jk == 0 || jk == 5 || jk == 6 || jk == 7)) {
+        const bool u8_slab = al && metric == KNNG_L2SQ && dt == KNNG_U8 && D.d <= kTcRowBytes && D.d % 16 == 0;
+        if (u8_slab && jk == 0) {
             // uint8 rows of one 128-B slab: Gram tiles on the tensor cores
             int* sqn = reinterpret_cast<int*>(ws + L.sqn);
             if (!sqn_ready) {
@@ -412,54 +409,22 @@ struct Run {
                 });
                 sqn_ready = true;
             }
-            if (!perm_ready && g_opt_join_order.load() && D.cap % 4 == 0 && D.d <= kOrderMaxD) {
-                // locality order of the joins (performance only, D17)
-                float* osum = reinterpret_cast<float*>(ws + L.osum);
-                uint32_t* ocode = reinterpret_cast<uint32_t*>(ws + L.ocode);
-                uint32_t* ohist = reinterpret_cast<uint32_t*>(ws + L.ohist);
-                uint32_t* operm = reinterpret_cast<uint32_t*>(ws + L.perm);
-                cudaMemsetAsync(osum, 0, static_cast<size_t>(D.d) * 4, c.stream);
-                cudaMemsetAsync(ohist, 0, static_cast<size_t>(kOrderBuckets) * 4, c.stream);
-                const uint8_t* Xu = static_cast<const uint8_t*>(X);
-                const int nb = static_cast<int>((D.n + 255) / 256);
-                c.launch("k_order_colsum",
-                         [&] { k_order_colsum<uint8_t><<<8 * sms, 128, 0, c.stream>>>(Xu, D.n, D.d, osum); });
-                c.launch("k_order_code", [&] {
-                    k_order_code<uint8_t><<<nb, 256, 0, c.stream>>>(Xu, D.n, D.d, osum, ocode, ohist);
-                });
-                c.launch("k_order_scan", [&] { k_order_scan<<<1, 256, 0, c.stream>>>(ohist); });
-                c.launch("k_order_scatter",
-                         [&] { k_order_scatter<<<nb, 256, 0, c.stream>>>(ocode, D.n, ohist, operm); });
-                perm_ready = true;
-            }
             unsigned long long* work = reinterpret_cast<unsigned long long*>(ws + L.flag + 8);
             cudaMemsetAsync(work, 0, 8, c.stream);
             c.launch("k_join", [&] {
                 constexpr size_t sm = TcCfg::kSmem;
-                const uint32_t* pm = perm_ready ? reinterpret_cast<const uint32_t*>(ws + L.perm) : nullptr;
                 CUtensorMap tm;
                 memset(&tm, 0, sizeof(tm));
-                const bool tma = jk == 0 && make_row_tmap(X, D.n, D.d, &tm);  // option 7: cp.async rows
+                // rows by TMA gather4; 16-B cp.async copies if the driver's
+                // tensor-map encoder is unavailable (bit-identical)
+                const bool tma = make_row_tmap(X, D.n, D.d, &tm);
                 auto go = [&](auto kfn, int ctas, int threads) {
                     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
                     kfn<<<ctas * sms, threads, sm, c.stream>>>(static_cast<const uint8_t*>(X), sqn, D, G, S, boundary,
-                                                               work, st, pm, tm);
+                                                               work, st, tm);
                 };
-                if (jk == 5) go(k_join_tc<4, 4, false>, 4, 5 * 32);       // 4 epilogue warps, 4 CTAs per SM
-                else if (jk == 6) go(k_join_tc<8, 4, false>, 4, 9 * 32);  // 8 epilogue warps, 4 CTAs per SM
-                else if (tma) go(k_join_tc<8, 3, true>, 3, 9 * 32);       // rows by TMA gather4
-                else go(k_join_tc<8, 3, false>, 3, 9 * 32);               // 8 epilogue warps, 3 CTAs per SM
-            });
-            return true;
-        }
-        if (u8_slab && jk == 3) {
-            // uint8 rows that fit one 128-B slab: lock-step pipeline, 2 CTAs/SM
-            unsigned long long* work = reinterpret_cast<unsigned long long*>(ws + L.flag + 8);
-            cudaMemsetAsync(work, 0, 8, c.stream);
-            c.launch("k_join", [&] {
-                constexpr size_t sm = LsCfg::kSmem;
-                cudaFuncSetAttribute(k_join_ls, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-                k_join_ls<<<2 * sms, kLsThreads, sm, c.stream>>>(static_cast<const uint8_t*>(X), D, G, S, boundary, work, st);
+                if (tma) go(k_join_tc<8, 3, true>, 3, 9 * 32);  // 8 epilogue warps, 3 CTAs per SM
+                else go(k_join_tc<8, 3, false>, 3, 9 * 32);
             });
             return true;
         }
@@ -504,45 +469,21 @@ struct Run {
             constexpr int STG = 5;
             unsigned long long* work = reinterpret_cast<unsigned long long*>(ws + L.flag + 8);
             cudaMemsetAsync(work, 0, 8, c.stream);
-            // float rows: 16-B cp.async copies by the gather warps; option
-            // join_kernel 8 stages them by TMA gather4 instead (bit-identical;
-            // measured no faster: DEEP-shaped 10.8 vs 10.9 ms, GIST-shaped
-            // 14.1 vs 12.4 ms per launch -- the consumers, not the copies,
-            // bound this kernel; profiles/r01s2_join_ws_tma.txt)
-            CUtensorMap tm;
-            memset(&tm, 0, sizeof(tm));
-            const float* Xf = metric == KNNG_COSINE ? Xn : static_cast<const float*>(X);
-            const bool tma = (metric == KNNG_COSINE || dt == KNNG_F32) && jk == 8 && D.d % 4 == 0 &&
-                             make_f32_slab_tmap(Xf, D.n, D.d, &tm);
             c.launch("k_join", [&] {
                 if (metric == KNNG_COSINE) {
                     constexpr size_t sm = WsCfg<float, true, STG>::kSmem;
-                    if (tma) {
-                        cudaFuncSetAttribute(k_join_ws<float, true, STG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(sm + 1024));
-                        k_join_ws<float, true, STG, true><<<sms, kWsThreads, sm + 1024, c.stream>>>(nullptr, Xn, D, G, S,
-                                                                                                    boundary, work, st, tm);
-                    } else {
-                        cudaFuncSetAttribute(k_join_ws<float, true, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-                        k_join_ws<float, true, STG><<<sms, kWsThreads, sm, c.stream>>>(nullptr, Xn, D, G, S, boundary, work, st, tm);
-                    }
+                    cudaFuncSetAttribute(k_join_ws<float, true, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+                    k_join_ws<float, true, STG><<<sms, kWsThreads, sm, c.stream>>>(nullptr, Xn, D, G, S, boundary, work, st);
                 } else if (dt == KNNG_F32) {
                     constexpr size_t sm = WsCfg<float, false, STG>::kSmem;
-                    if (tma) {
-                        cudaFuncSetAttribute(k_join_ws<float, false, STG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(sm + 1024));
-                        k_join_ws<float, false, STG, true><<<sms, kWsThreads, sm + 1024, c.stream>>>(
-                            static_cast<const float*>(X), nullptr, D, G, S, boundary, work, st, tm);
-                    } else {
-                        cudaFuncSetAttribute(k_join_ws<float, false, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-                        k_join_ws<float, false, STG><<<sms, kWsThreads, sm, c.stream>>>(static_cast<const float*>(X), nullptr,
-                                                                                        D, G, S, boundary, work, st, tm);
-                    }
+                    cudaFuncSetAttribute(k_join_ws<float, false, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+                    k_join_ws<float, false, STG><<<sms, kWsThreads, sm, c.stream>>>(static_cast<const float*>(X), nullptr,
+                                                                                    D, G, S, boundary, work, st);
                 } else {
                     constexpr size_t sm = WsCfg<uint8_t, false, STG>::kSmem;
                     cudaFuncSetAttribute(k_join_ws<uint8_t, false, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
                     k_join_ws<uint8_t, false, STG><<<sms, kWsThreads, sm, c.stream>>>(static_cast<const uint8_t*>(X), nullptr,
-                                                                                      D, G, S, boundary, work, st, tm);
+                                                                                      D, G, S, boundary, work, st);
                 }
             });
             return true;
@@ -649,6 +590,9 @@ knng_status get_workspace(Ctx& c, void* workspace, size_t bytes, size_t need, ch
     }
     if (bytes < need) return fail(KNNG_E_USAGE, "workspace too small: %zu < %zu bytes", bytes, need);
     if (!is_device_ptr(workspace)) return fail(KNNG_E_USAGE, "workspace is not a device pointer");
+    // the layout holds u64 arrays, 16-B vector loads and mbarrier words
+    if (reinterpret_cast<uintptr_t>(workspace) % 256 != 0)
+        return fail(KNNG_E_USAGE, "workspace must be 256-byte aligned");
     *out = static_cast<char*>(workspace);
     return KNNG_OK;
 }
@@ -966,18 +910,27 @@ knng_status knng_merge(const void* vecA, int64_t nA, const uint32_t* idsA, const
     R.compress();
     uint64_t* reserved = reinterpret_cast<uint64_t*>(ws + R.L.reserved);
     const int grid = R.warps_grid(n, 8);
+    int* bad = reinterpret_cast<int*>(ws + R.L.flag) + 1;
+    cudaMemsetAsync(bad, 0, 4, c.stream);
     c.launch("k_ggm_seed", [&] {
         if (metric == KNNG_COSINE)
             k_ggm_seed<float, true><<<grid, 256, 256 * 4, c.stream>>>(nullptr, R.Xn, R.D, nA, level, seed, idsA, distsA, idsB,
-                                                                distsB, R.G, reserved);
+                                                                distsB, R.G, reserved, bad);
         else if (R.dt == KNNG_F32)
             k_ggm_seed<float, false><<<grid, 256, 256 * 4, c.stream>>>(reinterpret_cast<const float*>(R.X), nullptr, R.D, nA,
-                                                                 level, seed, idsA, distsA, idsB, distsB, R.G, reserved);
+                                                                 level, seed, idsA, distsA, idsB, distsB, R.G, reserved, bad);
         else
             k_ggm_seed<uint8_t, false><<<grid, 256, 256 * 4, c.stream>>>(reinterpret_cast<const uint8_t*>(R.X), nullptr, R.D,
                                                                    nA, level, seed, idsA, distsA, idsB, distsB, R.G,
-                                                                   reserved);
+                                                                   reserved, bad);
     });
+    {
+        int h = 0;
+        cudaMemcpyAsync(&h, bad, 4, cudaMemcpyDeviceToHost, c.stream);
+        const cudaError_t e = cudaStreamSynchronize(c.stream);
+        if (c.err == cudaSuccess && e == cudaSuccess && h)
+            return fail(KNNG_E_USAGE, "input graph holds an id outside its own node range");
+    }
     for (int t = 0; t < merge_iters; ++t)
         R.iteration(t, 0x80000000u | (static_cast<uint32_t>(level) << 16) | static_cast<uint32_t>(t), t > 0);
     R.merge_sample(1, 0, merge_iters - 1);
@@ -1039,12 +992,8 @@ knng_status knng_set_option(const char* name, int64_t value) {
         g_opt_exact_u8.store(value ? 1 : 0);
         return KNNG_OK;
     }
-    if (strcmp(name, "join_order") == 0) {
-        g_opt_join_order.store(value ? 1 : 0);
-        return KNNG_OK;
-    }
     if (strcmp(name, "join_kernel") == 0) {
-        if (value < 0 || value > 8) return fail(KNNG_E_USAGE, "join_kernel must be in [0, 8]");
+        if (value < 0 || value > 4 || value == 3) return fail(KNNG_E_USAGE, "join_kernel must be 0, 1, 2 or 4");
         g_opt_join_kernel.store(static_cast<int>(value));
         return KNNG_OK;
     }
@@ -1055,7 +1004,6 @@ knng_status knng_get_option(const char* name, int64_t* host_value) {
     if (!name || !host_value) return fail(KNNG_E_USAGE, "null argument");
     if (strcmp(name, "exact_u8") == 0) *host_value = g_opt_exact_u8.load();
     else if (strcmp(name, "join_kernel") == 0) *host_value = g_opt_join_kernel.load();
-    else if (strcmp(name, "join_order") == 0) *host_value = g_opt_join_order.load();
     else if (strcmp(name, "last_exact_u8") == 0) *host_value = g_last_exact_u8;
     else return fail(KNNG_E_USAGE, "unknown option '%s'", name);
     return KNNG_OK;

@@ -169,6 +169,17 @@ def knng_merge(vecA, idsA, distsA, vecB, idsB, distsB, k: int, merge_iters: int,
     nA, d = vecA.shape
     nB = vecB.shape[0]
     dt = _dtype_code(vecA)
+    # the C side trusts these shapes (it copies nB * d elements of vecB and
+    # reads k entries per list): check them here
+    if vecB.dim() != 2 or vecB.shape[1] != d or vecA.dtype != vecB.dtype:
+        raise ValueError(f"vecB must be [nB, {d}] of dtype {vecA.dtype}, got {tuple(vecB.shape)} {vecB.dtype}")
+    for name, t, rows, dtypes in (("idsA", idsA, nA, ("int32", "uint32")), ("distsA", distsA, nA, ("float32",)),
+                                  ("idsB", idsB, nB, ("int32", "uint32")), ("distsB", distsB, nB, ("float32",))):
+        if tuple(t.shape) != (rows, k) or not any(str(t.dtype).endswith(x) for x in dtypes):
+            raise ValueError(f"{name} must be [{rows}, {k}] {dtypes[0]}, got {tuple(t.shape)} {t.dtype}")
+    for t in (vecA, vecB, idsA, distsA, idsB, distsB):
+        if not (t.is_cuda and t.is_contiguous()):
+            raise ValueError("knng_merge needs contiguous CUDA tensors")
     out_ids = torch.empty((nA + nB, k), dtype=torch.int32, device=vecA.device)
     out_dists = torch.empty((nA + nB, k), dtype=torch.float32, device=vecA.device)
     ws_ptr, ws_bytes = None, 0

@@ -111,10 +111,25 @@ def knng_build_sharded(local_vectors, shards: int, k: int, iters: int, merge_ite
     (host-side order of events, for tests)."""
     import torch
 
+    # every copy, exchange and library call of the tree runs on one stream:
+    # the ops' stream when it is a torch stream, else the current one
+    ops = ops or CudaOps()
+    st = getattr(ops, "stream", None)
+    if st is not None and local_vectors.is_cuda and hasattr(st, "cuda_stream"):
+        with torch.cuda.stream(st):
+            return _build_sharded(local_vectors, shards, k, iters, merge_iters, sample_size, seed, metric, group,
+                                  ops, scatter, timeline)
+    return _build_sharded(local_vectors, shards, k, iters, merge_iters, sample_size, seed, metric, group, ops,
+                          scatter, timeline)
+
+
+def _build_sharded(local_vectors, shards, k, iters, merge_iters, sample_size, seed, metric, group, ops, scatter,
+                   timeline):
+    import torch
+
     comm = _Comm(group)
     world = comm.dist.get_world_size(group) if comm.active else 1
     rank = comm.dist.get_rank(group) if comm.active else 0
-    ops = ops or CudaOps()
     n_local, d = local_vectors.shape
     per = shards // world
     if shards % world or n_local % per:

@@ -117,3 +117,58 @@ def test_fullsize_iteration_sampled_targets(K, c2):
     assert (gk[:, 1:] > gk[:, :-1]).all()
     assert (orc.key_ids(gk) != np.arange(len(X), dtype=np.uint32)[:, None]).all()
     assert (orc.key_dists(gk) <= orc.key_dists(keys0)).all()
+
+
+# ------------------------------------------------- full size, float rows (C4 shape)
+def test_fullsize_deep_iteration_sampled_targets(K):
+    # DEEP-shaped continuous fp32 rows at 1M x 96 (the C4 shard shape; the
+    # float join k_join_ws, not the exact-u8 path), one iteration from an
+    # oracle state; the oracle evaluates 1500 sampled targets.
+    X = datagen.make("deep", 1_000_000, seed=2)
+    keys0, _ = orc.init(X, 32, 42)
+    rng = np.random.default_rng(4)
+    flags0 = (rng.random(keys0.shape) < 0.4).astype(np.uint8)
+    targets = datagen.sample_nodes(len(X), 1500, seed=9)
+    mask = np.zeros(len(X), np.uint8)
+    mask[targets] = 1
+    ok, of = keys0.copy(), flags0.copy()
+    orc.iterate(X, ok, of, 16, 2, 42, target_mask=mask)
+    gk, gf = dev(keys0.view(np.int64)), dev(flags0)
+    st = K.knng_debug_iterate(dev(X), gk, gf, 16, 2, 42)
+    assert K.knng_get_option("last_exact_u8") == 0
+    gk, gf = u64(gk), gf.cpu().numpy()
+    assert np.array_equal(gk[targets], ok[targets])
+    assert np.array_equal(gf[targets], of[targets])
+    assert st["joins"] > 900_000
+    assert (gk[:, 1:] > gk[:, :-1]).all()
+    assert (orc.key_dists(gk) <= orc.key_dists(keys0)).all()
+
+
+def test_fullsize_ggm_2x500k_restricted_iteration_sampled_targets(K, c2):
+    # the bench's GGM shape: C2 split into 2 x 500k.  Input graphs: each
+    # half's random init (oracle), seeded by the oracle's GGM seed step; one
+    # restricted refine iteration (boundary = 500k) on the GPU equals the
+    # oracle's on 2000 sampled targets.
+    X = c2[0]
+    h = len(X) // 2
+    ka, _ = orc.init(X[:h], 32, 5)
+    kb, _ = orc.init(X[h:], 32, 6)
+    keys_in = np.concatenate([ka, orc.key(orc.key_dists(kb), orc.key_ids(kb).astype(np.uint64) + np.uint64(h))])
+    keys, flags, _ = orc.ggm_seed(X, keys_in, h, 32, 77, level=0)
+    targets = datagen.sample_nodes(len(X), 2000, seed=10)
+    mask = np.zeros(len(X), np.uint8)
+    mask[targets] = 1
+    tword = 0x80000000 | 1
+    ok, of = keys.copy(), flags.copy()
+    ost = orc.iterate(X, ok, of, 16, tword, 77, boundary=h, target_mask=mask)
+    gk, gf = dev(keys.view(np.int64)), dev(flags)
+    st = K.knng_debug_iterate(dev(X), gk, gf, 16, tword, 77, h)
+    gk, gf = u64(gk), gf.cpu().numpy()
+    assert np.array_equal(gk[targets], ok[targets])
+    assert np.array_equal(gf[targets], of[targets])
+    assert st["joins"] > 900_000 and ost["joins"] > 0
+    # lists never get worse, and every entry a refine inserted is cross-subset
+    assert (orc.key_dists(gk) <= orc.key_dists(keys)).all()
+    for t in targets[:500]:
+        fresh = set(orc.key_ids(gk[t]).tolist()) - set(orc.key_ids(keys[t]).tolist())
+        assert all((v >= h) != (t >= h) for v in fresh)

@@ -265,3 +265,68 @@ def test_usage_errors():
         orc.build(X, 4, 4, 1, 1)    # p >= k
     with pytest.raises(RuntimeError):
         orc.build(X, 4, 0, 1, 1)    # p < 1
+
+
+# ------------------------------------- restricted (GGM refine) iteration, brute force
+@pytest.mark.parametrize("n,nA,d,k,p,seed", [(80, 30, 4, 6, 2, 0), (120, 70, 6, 10, 4, 1), (100, 50, 3, 8, 7, 2)])
+def test_restricted_iteration_matches_bruteforce_definition(n, nA, d, k, p, seed):
+    # GGM refine (D22 membership reading): the same Alg. 1
+    # body with every pair (a, b), (a >= nA) == (b >= nA), skipped.  States:
+    # the oracle's GGM seed of two built halves, then a random NEW/OLD mix.
+    X = datagen.make("c1", n, seed=seed, d=d)
+    ia, da = orc.build(X[:nA], k, p, 3, seed)
+    ib, db = orc.build(X[nA:], k, p, 3, seed + 1)
+    keys_in = np.concatenate([orc.key(da, ia), orc.key(db, ib.astype(np.uint64) + np.uint64(nA))])
+    keys, flags, _ = orc.ggm_seed(X, keys_in, nA, k, seed, level=1)
+    rng = np.random.default_rng(seed)
+    for t in range(4):
+        if t == 2:
+            flags = (rng.random(flags.shape) < 0.5).astype(np.uint8)
+        tword = 0x80000000 | (1 << 16) | t
+        ek, ef = _iterate_bruteforce(X, keys, flags, p, tword, seed, boundary=nA)
+        st = orc.iterate(X, keys, flags, p, tword, seed, boundary=nA)
+        assert np.array_equal(keys, ek), f"iteration {t}"
+        assert np.array_equal(flags, ef), f"iteration {t}"
+        assert st["dist_evals"] >= 0
+
+
+def _merge_bruteforce(X, keys_in, nA, k, p, merge_iters, seed, level):
+    """Alg. 3 from its definition: the oracle's seed step (pinned by SPEC
+    S:264-266 in test_oracle_ggm_eval.py), merge_iters restricted iterations
+    evaluated by _iterate_bruteforce, finalize as the k smallest unique keys
+    of refined U reserved."""
+    keys, flags, reserved = orc.ggm_seed(X, keys_in, nA, k, seed, level=level)
+    for t in range(merge_iters):
+        tword = 0x80000000 | (level << 16) | t
+        keys, flags = _iterate_bruteforce(X, keys, flags, p, tword, seed, boundary=nA)
+    out = keys.copy()
+    for i in range(len(X)):
+        out[i] = np.array(sorted(set(int(x) for x in keys[i]) | set(int(x) for x in reserved[i]))[:k], np.uint64)
+    return out
+
+
+def test_tree_build_equals_explicit_two_level_composition():
+    # Log-depth tree (D26, D36): 4 contiguous shards, shard g built with seed
+    # + g on local ids; level 0 merges (0,1) and (2,3), level 1 merges
+    # (01, 23); each merge numbers its ids from the group's first row and
+    # uses Philox level l; ids are re-based to global after every merge.
+    # The merges here are the brute-force definition above, not orc.merge.
+    S, ns, k, p, iters, mi, seed = 4, 40, 6, 3, 3, 2, 5
+    X = datagen.make("c1", S * ns, seed=12, d=4)
+    shard = []
+    for g in range(S):
+        ids, dists = orc.build(X[g * ns:(g + 1) * ns], k, p, iters, seed + g)
+        shard.append(orc.key(dists, ids))  # local ids
+
+    def merge_pair(XA, KA, XB, KB, level):
+        nA = len(XA)
+        kin = np.concatenate([KA, orc.key(orc.key_dists(KB), orc.key_ids(KB).astype(np.uint64) + np.uint64(nA))])
+        return _merge_bruteforce(np.concatenate([XA, XB]), kin, nA, k, p, mi, seed, level)
+
+    l01 = merge_pair(X[:ns], shard[0], X[ns:2 * ns], shard[1], 0)
+    l23 = merge_pair(X[2 * ns:3 * ns], shard[2], X[3 * ns:], shard[3], 0)
+    top = merge_pair(X[:2 * ns], l01, X[2 * ns:], l23, 1)
+    got = orc.tree_build(X, S, k, p, iters, mi, seed)
+    assert np.array_equal(got, top)
+    # and a wrong level or seed changes the result (the pin is sensitive)
+    assert not np.array_equal(got, orc.tree_build(X, S, k, p, iters, mi, seed + 1))
