@@ -1,7 +1,7 @@
 # Builds the CUDA product library (sm_100a) and the C oracle (test infra).
 NVCC      ?= nvcc
 ARCH      := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS   := -O3 -std=c++17 $(ARCH) -lineinfo --fmad=false -Xcompiler -fPIC,-Wall -shared
+NVFLAGS   := -O3 -std=c++17 $(ARCH) -lineinfo --fmad=false -Xcompiler -fPIC,-Wall -shared -ldl
 PKG       := paper_2103_15386_b200
 LIB       := $(PKG)/lib/libknng.so
 SRCS      := $(wildcard $(PKG)/csrc/*.cu $(PKG)/csrc/*.cuh) include/knng.h

@@ -47,7 +47,7 @@ typedef enum {
                             under cosine)                                    */
     KNNG_E_NOMEM = 3,    /* workspace too small / device allocation failed  */
     KNNG_E_CUDA = 4,     /* CUDA runtime error (message in knng_last_error) */
-    KNNG_E_NCCL = 5,     /* reserved for the sharded build                  */
+    KNNG_E_NCCL = 5,     /* NCCL / exchange failure (multi-GPU entry points) */
     KNNG_E_INTERNAL = 6
 } knng_status;
 
@@ -126,16 +126,59 @@ knng_status knng_merge(const void* vecA, int64_t nA, const uint32_t* idsA,
                        size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------------------------
- * Sharded build (D26, D36, section 11).  There is no
- * separate C entry point: the multi-GPU build is knng_build on every shard
- * (shard g of S built with seed + g, local ids) followed by knng_merge per
- * tree level (level l merges groups of 2^(l+1) shards, ids numbered from the
- * group's first row, Philox level l).  The exchange between GPUs is one
- * point-to-point block transfer (vectors, ids, dists) per level, done by
- * paper_2103_15386_b200/sharded.py over torch.distributed (NCCL on NVLink);
- * knng_merge uses the received rows in place when they follow the leader's
- * own (D37).  The result depends only on S, not on the number of GPUs.
+ * Multi-GPU (one process -- or one host thread -- per GPU).
+ * The paper builds sub-graphs of the shards on different GPUs and merges
+ * them with GGM ("GGM allows the k-NN graph to be built on multiple
+ * GPUs simultaneously"; "multiple merges can be run on multiple
+ * GPUs").  DESIGN.md section 11, D26/D36.
+ *
+ * knng_get_unique_id: the NCCL unique id (128 bytes, host) that rank 0
+ *   creates and the caller broadcasts (torch.distributed's only role).
+ * knng_comm_init: NCCL communicator of this rank (ncclCommInitRank; libnccl
+ *   is loaded with dlopen here).  *comm receives an opaque handle.  The
+ *   calling thread's current device is the rank's GPU.  KNNG_E_NCCL if NCCL
+ *   is unavailable or fails.
+ * knng_comm_init_local: `world` communicators of ranks that are host THREADS
+ *   of this process (host_comms[world] receives the handles); messages are
+ *   device copies after CUDA events.  Any device per rank, including several
+ *   ranks on one GPU -- the parity tests run the whole distributed path this
+ *   way on one B200.
+ * knng_comm_destroy: frees a handle of either kind.
+ *
+ * knng_build_sharded -- collective over the communicator: rank r holds the
+ *   global rows [r n_local, (r+1) n_local) (contiguous, equal shards).
+ *   1. GNND (knng_build) on the own shard with seed + r;
+ *   2. log-depth GGM tree (D26): level l = 0 .. log2(world)-1 merges every
+ *      group of 2^(l+1) ranks (left half = A) with its ids numbered from the
+ *      group's first row, Philox level l, and merge iterations
+ *      host_level_iters[l] (or merge_iters for every level when NULL).  Every
+ *      rank of the group takes part: it keeps the lists, samples and buckets
+ *      of its own rows; forward samples travel as reverse records to
+ *      the targets' owners, the k-th keys (D17) are gathered, join
+ *      candidates travel as (target, key) records to the owners, who file
+ *      them (grouped point-to-point exchanges on NVLink); the group's vectors
+ *      are replicated once per level.
+ *   The result is bit-identical to the one-GPU log-depth tree of `world`
+ *   shards (oracle tree_build), i.e. independent of the transport.
+ *   local_vectors  [n_local][d] device;  out_ids_local / out_dists_local
+ *   [n_local][k] device: the own rows' lists with GLOBAL ids.
+ *   Requires: world a power of two; n_total == world * n_local;
+ *   global_offset == rank * n_local; identical parameters on every rank
+ *   (checked collectively -> KNNG_E_USAGE on every rank); n_total < 2^32-1.
+ *   A rank that fails after the collective checks leaves its peers waiting
+ *   (as NCCL does).  Counters: knng_last_stats returns the shard build's
+ *   iterations followed by every level's refine iterations (this rank's
+ *   joins).
  * ---------------------------------------------------------------------- */
+knng_status knng_get_unique_id(void* host_out128);
+knng_status knng_comm_init(int32_t rank, int32_t world, const void* host_id128, void** comm);
+knng_status knng_comm_init_local(int32_t world, void** host_comms);
+knng_status knng_comm_destroy(void* comm);
+knng_status knng_build_sharded(void* comm, const void* local_vectors, int64_t n_local, int64_t global_offset,
+                               int64_t n_total, knng_dtype dt, int32_t d, int32_t k, knng_metric metric,
+                               int32_t iters, int32_t merge_iters, const int32_t* host_level_iters,
+                               int32_t sample_size, uint64_t seed, uint32_t* out_ids_local,
+                               float* out_dists_local, void* stream);
 
 /* ------------------------------------------------------------------------
  * knng_bruteforce -- exact top-kq neighbours (j != q) of nq query rows by

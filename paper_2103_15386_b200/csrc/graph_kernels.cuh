@@ -22,6 +22,16 @@ struct Graph {
     uint32_t* bcnt;     // [n]    candidates appended to t's bucket
     const uint64_t* boff;  // [n+1] bucket offsets (= Samples::off channel 2)
     uint64_t* bucket;   // [6 n p] candidate keys of the current iteration
+    // The joins read the threshold of target t at kth_t[t] (t: a sample id).
+    // One GPU: kth_t == kth.  Distributed refine (dist_kernels.cuh): kth_t
+    // is the group-wide copy, gathered every iteration.
+    const uint64_t* kth_t;
+    // Record mode (distributed refine): instead of appending into the local
+    // buckets, the joins write (target, key) records at rec_tgt/rec_key[slot],
+    // slot from the counter rec_cnt; nullptr = bucket mode.
+    uint32_t* rec_tgt;
+    uint64_t* rec_key;
+    unsigned long long* rec_cnt;
 };
 
 struct Samples {
@@ -30,7 +40,8 @@ struct Samples {
     uint32_t* rcnt;  // [2][n]      reverse counts
     uint32_t* fpos;  // [2][n][p]   slot of forward sample (s, j) in its target's reverse list
     uint64_t* off;   // [3][n+1]    CSR offsets: reverse NEW, reverse OLD, buckets
-    uint32_t* rsrc;  // [2][n*p]    reverse sources
+    uint32_t* rsrc;  // [2][rstride] reverse sources
+    int64_t rstride; // n*p (one GPU) or the received-record bound (distributed)
     uint32_t* G;     // [2][n][cap] G_new / G_old, sorted unique
     uint8_t* gcnt;   // [n][2]      m = |G_new|, q = |G_old|
     uint64_t* bsum;  // [3][nblk]   scan block sums
@@ -38,8 +49,9 @@ struct Samples {
 };
 
 struct Dims {
-    int64_t n;
+    int64_t n;          // nodes whose lists this launch owns
     int d, k, p, cap;
+    int64_t base = 0;   // id of the first owned node (distributed refine; else 0)
 };
 
 __device__ __forceinline__ uint32_t kmask_of(int k) { return k >= 32 ? kFull : ((1u << k) - 1u); }
@@ -200,15 +212,18 @@ __global__ void __launch_bounds__(256, 8) k_merge_sample(Dims D, Graph G, Sample
         const int rn = __popc(newb & lanemask_lt());
         const int ro = __popc(oldb & lanemask_lt());
         const uint32_t id = key_id(cur.key);
+        // the count's old value is the sample's slot in the reverse CSR (one
+        // GPU; a distributed refine sends the forward samples to the targets'
+        // owners instead, S.fpos == nullptr)
         if (isnew && rn < p) {
             S.fwd[static_cast<size_t>(s) * p + rn] = id;
-            // the count's old value is this sample's slot in the reverse CSR
-            S.fpos[static_cast<size_t>(s) * p + rn] = atomicAdd(S.rcnt + id, 1u);
+            if (S.fpos) S.fpos[static_cast<size_t>(s) * p + rn] = atomicAdd(S.rcnt + id, 1u);
             cur.meta &= ~1u;  // "Mark all sampled neighbors as OLD"
         }
         if (isold && ro < p) {
             S.fwd[static_cast<size_t>(D.n) * p + static_cast<size_t>(s) * p + ro] = id;
-            S.fpos[static_cast<size_t>(D.n) * p + static_cast<size_t>(s) * p + ro] = atomicAdd(S.rcnt + D.n + id, 1u);
+            if (S.fpos)
+                S.fpos[static_cast<size_t>(D.n) * p + static_cast<size_t>(s) * p + ro] = atomicAdd(S.rcnt + D.n + id, 1u);
         }
         if (lane == 0) {
             S.fcnt[2 * s] = static_cast<uint8_t>(min(__popc(newb), p));
@@ -310,7 +325,7 @@ __global__ void k_rev_scatter(Dims D, Samples S) {
     if (j >= S.fcnt[2 * s + f]) return;
     const uint32_t v = S.fwd[static_cast<size_t>(f) * D.n * D.p + i];
     const uint32_t pos = S.fpos[static_cast<size_t>(f) * D.n * D.p + i];
-    S.rsrc[static_cast<size_t>(f) * D.n * D.p + S.off[f * (D.n + 1) + v] + pos] = static_cast<uint32_t>(s);
+    S.rsrc[static_cast<size_t>(f) * S.rstride + S.off[f * (D.n + 1) + v] + pos] = static_cast<uint32_t>(s);
 }
 
 // sort + dedup one u32 id per lane (0xFFFFFFFF = empty, sorts last); returns
@@ -344,7 +359,7 @@ __device__ __forceinline__ bool rev_select_ties(uint32_t src, int r, int f, uint
     if (static_cast<int>(lane) < r) {
         const uint4 o =
             philox4x32_10(make_uint4(f == 0 ? kTagRevNew : kTagRevOld, tword, src, static_cast<uint32_t>(v)), key);
-        pr = (o.x & ~31u) | lane;
+        pr = (o.x & ~31u) | lane;  // (v: the node's id, D.base + local index)
     }
     pr = warp_sort_u32(pr);
     const uint32_t prev = __shfl_sync(kFull, pr, (lane + 31) & 31);
@@ -365,6 +380,7 @@ __device__ __forceinline__ bool rev_select_ties(uint32_t src, int r, int f, uint
 __global__ void __launch_bounds__(256, 8) k_rev_select(Dims D, Samples S, uint32_t tword, uint64_t seed) {
     const int64_t v = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (v >= D.n) return;
+    const int64_t vid = D.base + v;  // the node's id (the Philox priority word)
     const uint32_t lane = lane_id();
     const uint2 key = seed_key(seed);
     const int p = D.p, cap = D.cap;
@@ -387,11 +403,11 @@ __global__ void __launch_bounds__(256, 8) k_rev_select(Dims D, Samples S, uint32
     }
 #pragma unroll
     for (int f = 0; f < 2; ++f)
-        pre[f] = static_cast<int>(lane) < rv[f] ? S.rsrc[static_cast<size_t>(f) * D.n * p + o0v[f] + lane] : 0xFFFFFFFFu;
+        pre[f] = static_cast<int>(lane) < rv[f] ? S.rsrc[static_cast<size_t>(f) * S.rstride + o0v[f] + lane] : 0xFFFFFFFFu;
 #pragma unroll
     for (int f = 0; f < 2; ++f) {
         const int fc = fcv[f];
-        const uint32_t* rs = S.rsrc + static_cast<size_t>(f) * D.n * p;
+        const uint32_t* rs = S.rsrc + static_cast<size_t>(f) * S.rstride;
         const uint64_t o0 = o0v[f];
         const int r = rv[f];
         const int c = cap - fc;
@@ -401,7 +417,7 @@ __global__ void __launch_bounds__(256, 8) k_rev_select(Dims D, Samples S, uint32
             const int j = static_cast<int>(lane) - fc;
             const uint32_t got = __shfl_sync(kFull, pre[f], j >= 0 && j < r ? j : 0);
             if (j >= 0 && j < r) e = got;
-        } else if (r <= 32 && !rev_select_ties(pre[f], r, f, tword, v, key, fc, c, e)) {
+        } else if (r <= 32 && !rev_select_ties(pre[f], r, f, tword, vid, key, fc, c, e)) {
             // selected by the 32-bit fast path (no priority ties)
         } else {
             uint64_t best = kSentinel;  // running 32 smallest (prio, s), sorted
@@ -410,7 +426,7 @@ __global__ void __launch_bounds__(256, 8) k_rev_select(Dims D, Samples S, uint32
                 if (base + static_cast<int>(lane) < r) {
                     const uint32_t src = base == 0 ? pre[f] : rs[o0 + base + lane];
                     const uint4 o = philox4x32_10(
-                        make_uint4(f == 0 ? kTagRevNew : kTagRevOld, tword, src, static_cast<uint32_t>(v)), key);
+                        make_uint4(f == 0 ? kTagRevNew : kTagRevOld, tword, src, static_cast<uint32_t>(vid)), key);
                     x = (static_cast<uint64_t>(o.x) << 32) | src;
                 }
                 x = warp_sort_u64(x);

@@ -372,10 +372,16 @@ __global__ void k_cand_scatter(Dims D, Graph G, Samples S, DevStats* __restrict_
                 const uint32_t t = j < 2 * m
                     ? S.G[static_cast<size_t>(x) * D.cap + (j < m ? j : j - m)]
                     : S.G[static_cast<size_t>(D.n) * D.cap + static_cast<size_t>(x) * D.cap + (j - 2 * m)];
-                if (key < G.kth[t]) {  // else it cannot enter G[t] (exact, D17)
+                if (key < G.kth_t[t]) {  // else it cannot enter G[t] (exact, D17)
                     atomicAdd(&c_app, 1u);
-                    const uint32_t slot = atomicAdd(G.bcnt + t, 1u);
-                    G.bucket[G.boff[t] + slot] = key;
+                    if (G.rec_cnt) {  // record mode (distributed refine)
+                        const unsigned long long slot = atomicAdd(G.rec_cnt, 1ull);
+                        G.rec_key[slot] = key;
+                        G.rec_tgt[slot] = t;
+                    } else {
+                        const uint32_t slot = atomicAdd(G.bcnt + t, 1u);
+                        G.bucket[G.boff[t] + slot] = key;
+                    }
                 }
             }
         }

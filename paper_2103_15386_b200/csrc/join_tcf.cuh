@@ -276,6 +276,7 @@ k_join_tcf(const float* __restrict__ X, const float* __restrict__ sqn, Dims D, G
     uint64_t f1_key[2], f1_th = 0, f1_bo = 0;
     uint32_t f1_tgt = 0;
     uint64_t f2_key[2], f2_pos[2];
+    uint32_t f2_tgt = 0;
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
         f1_key[r] = kSentinel;
@@ -286,13 +287,30 @@ k_join_tcf(const float* __restrict__ X, const float* __restrict__ sqn, Dims D, G
     auto file_store = [&]() {
 #pragma unroll
         for (int r = 0; r < 2; ++r)
-            if (f2_key[r] != kSentinel) G.bucket[f2_pos[r]] = f2_key[r];
+            if (f2_key[r] != kSentinel) {
+                if (G.rec_cnt) {  // record mode (distributed refine)
+                    G.rec_key[f2_pos[r]] = f2_key[r];
+                    G.rec_tgt[f2_pos[r]] = f2_tgt;
+                } else {
+                    G.bucket[f2_pos[r]] = f2_key[r];
+                }
+            }
     };
     auto file_atomic = [&]() {
         const bool ok0 = f1_key[0] < f1_th, ok1 = f1_key[1] < f1_th;  // D17
         n_app += ok0 + ok1;
-        uint32_t sl = 0;
-        if (ok0 || ok1) sl = atomicAdd(G.bcnt + f1_tgt, static_cast<uint32_t>(ok0 + ok1));
+        uint64_t sl = 0;
+        if (G.rec_cnt) {
+            // record slots: one atomic per warp (the call is warp-uniform)
+            const uint32_t b0 = __ballot_sync(kFull, ok0), b1 = __ballot_sync(kFull, ok1);
+            unsigned long long wb = 0;
+            if (lane == 0 && (b0 | b1)) wb = atomicAdd(G.rec_cnt, static_cast<unsigned long long>(__popc(b0) + __popc(b1)));
+            sl = shfl_u64(wb, 0) + __popc(b0 & lanemask_lt()) + __popc(b1 & lanemask_lt());
+            f1_bo = 0;
+            f2_tgt = f1_tgt;
+        } else if (ok0 || ok1) {
+            sl = atomicAdd(G.bcnt + f1_tgt, static_cast<uint32_t>(ok0 + ok1));
+        }
         f2_key[0] = ok0 ? f1_key[0] : kSentinel;
         f2_pos[0] = f1_bo + sl;
         f2_key[1] = ok1 ? f1_key[1] : kSentinel;
@@ -459,8 +477,8 @@ k_join_tcf(const float* __restrict__ X, const float* __restrict__ sqn, Dims D, G
             f1_tgt = my_id;
             n_cand += (f1_key[0] != kSentinel) + (f1_key[1] != kSentinel);
             if (f1_key[0] != kSentinel || f1_key[1] != kSentinel) {  // D15
-                f1_th = __ldg(G.kth + my_id);
-                f1_bo = __ldg(G.boff + my_id);
+                f1_th = __ldg(G.kth_t + my_id);
+                if (!G.rec_cnt) f1_bo = __ldg(G.boff + my_id);
             }
             // rows(b) are no longer read by this warp: after every warp is
             // here (named barrier at the top of b+1 orders it), gather b+2

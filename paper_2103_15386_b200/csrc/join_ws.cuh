@@ -286,9 +286,28 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
                 th[r] = 0;
                 bo[r] = 0;
                 if (kv[r] != kSentinel) {  // D15: (inf, inf) inserts nothing
-                    th[r] = __ldg(G.kth + tg[r]);
-                    bo[r] = __ldg(G.boff + tg[r]);
+                    th[r] = __ldg(G.kth_t + tg[r]);
+                    if (!G.rec_cnt) bo[r] = __ldg(G.boff + tg[r]);
                 }
+            }
+            if (G.rec_cnt) {
+                // record mode (distributed refine): (target, key) records,
+                // one slot atomic per warp and round (warp-uniform loop)
+#pragma unroll
+                for (int r = 0; r < kEpiRounds; ++r) {
+                    n_cand += kv[r] != kSentinel;
+                    const bool ok = kv[r] != kSentinel && kv[r] < th[r];
+                    n_app += ok;
+                    const uint32_t b = __ballot_sync(kFull, ok);
+                    unsigned long long wb = 0;
+                    if (lane == 0 && b) wb = atomicAdd(G.rec_cnt, static_cast<unsigned long long>(__popc(b)));
+                    const uint64_t slot = shfl_u64(wb, 0) + __popc(b & lanemask_lt());
+                    if (ok) {
+                        G.rec_key[slot] = kv[r];
+                        G.rec_tgt[slot] = tg[r];
+                    }
+                }
+                continue;
             }
 #pragma unroll
             for (int r = 0; r < kEpiRounds; ++r) {

@@ -4,6 +4,7 @@
 #include <cudaTypedefs.h>
 
 #include <atomic>
+#include <functional>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -13,6 +14,8 @@
 #include <vector>
 
 #include "../../include/knng.h"
+#include "comm.cuh"
+#include "dist_kernels.cuh"
 #include "eval_kernels.cuh"
 #include "ggm_kernels.cuh"
 #include "join_kernel.cuh"
@@ -247,6 +250,8 @@ struct Run {
     uint64_t seed;
     int64_t boundary = -1;
     bool sqn_ready = false;   // L.sqn holds the exact squared norms of X
+    int64_t xrows = -1;       // rows of X (ids the samples may hold); -1: D.n
+    void* sqn_ext = nullptr;  // squared norms of all xrows rows (distributed refine), else L.sqn
     int sms = 148;            // SM count of the current device (persistent grids)
 
     Run(Ctx& ctx) : c(ctx) {
@@ -270,11 +275,16 @@ struct Run {
         S.fpos = reinterpret_cast<uint32_t*>(ws + L.fpos);
         S.off = reinterpret_cast<uint64_t*>(ws + L.off);
         S.rsrc = reinterpret_cast<uint32_t*>(ws + L.rsrc);
+        S.rstride = D.n * D.p;
         S.G = reinterpret_cast<uint32_t*>(ws + L.G);
         S.gcnt = reinterpret_cast<uint8_t*>(ws + L.gcnt);
         S.bsum = reinterpret_cast<uint64_t*>(ws + L.bsum);
         S.cand = L.has_cand ? reinterpret_cast<uint64_t*>(ws + L.cand) : nullptr;
         G.boff = S.off + 2 * (D.n + 1);
+        G.kth_t = G.kth;
+        G.rec_tgt = nullptr;
+        G.rec_key = nullptr;
+        G.rec_cnt = nullptr;
         stats = reinterpret_cast<DevStats*>(ws + L.stats);
         Xn = metric == KNNG_COSINE ? reinterpret_cast<const float*>(ws + L.xnorm) : nullptr;
     }
@@ -401,11 +411,12 @@ struct Run {
         const bool u8_slab = al && metric == KNNG_L2SQ && dt == KNNG_U8 && D.d <= kTcRowBytes && D.d % 16 == 0;
         if (u8_slab && jk == 0) {
             // uint8 rows of one 128-B slab: Gram tiles on the tensor cores
-            int* sqn = reinterpret_cast<int*>(ws + L.sqn);
+            int* sqn = static_cast<int*>(sqn_ext ? sqn_ext : ws + L.sqn);
+            const int64_t xr = xrows >= 0 ? xrows : D.n;
             if (!sqn_ready) {
                 c.launch("k_sqnorm_u8", [&] {
-                    k_sqnorm_u8<<<static_cast<int>((D.n + 255) / 256), 256, 0, c.stream>>>(
-                        static_cast<const uint8_t*>(X), D.n, D.d, sqn);
+                    k_sqnorm_u8<<<static_cast<int>((xr + 255) / 256), 256, 0, c.stream>>>(
+                        static_cast<const uint8_t*>(X), xr, D.d, sqn);
                 });
                 sqn_ready = true;
             }
@@ -417,7 +428,7 @@ struct Run {
                 memset(&tm, 0, sizeof(tm));
                 // rows by TMA gather4; 16-B cp.async copies if the driver's
                 // tensor-map encoder is unavailable (bit-identical)
-                const bool tma = make_row_tmap(X, D.n, D.d, &tm);
+                const bool tma = make_row_tmap(X, xr, D.d, &tm);
                 auto go = [&](auto kfn, int ctas, int threads) {
                     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
                     kfn<<<ctas * sms, threads, sm, c.stream>>>(static_cast<const uint8_t*>(X), sqn, D, G, S, boundary,
@@ -436,10 +447,11 @@ struct Run {
             // for the CUDA-core join (profiles/r01s2_ncu_k_join_tcf_deep.txt),
             // so the automatic choice stays on k_join_ws for float rows.
             const float* Xf = metric == KNNG_COSINE ? Xn : static_cast<const float*>(X);
-            float* sqn = reinterpret_cast<float*>(ws + L.sqn);
+            float* sqn = static_cast<float*>(sqn_ext ? sqn_ext : ws + L.sqn);
+            const int64_t xr = xrows >= 0 ? xrows : D.n;
             if (!sqn_ready) {
                 c.launch("k_sqnorm_f32", [&] {
-                    k_sqnorm_f32<<<static_cast<int>((D.n + 255) / 256), 256, 0, c.stream>>>(Xf, D.n, D.d, sqn);
+                    k_sqnorm_f32<<<static_cast<int>((xr + 255) / 256), 256, 0, c.stream>>>(Xf, xr, D.d, sqn);
                 });
                 sqn_ready = true;
             }
@@ -596,6 +608,8 @@ knng_status get_workspace(Ctx& c, void* workspace, size_t bytes, size_t need, ch
     *out = static_cast<char*>(workspace);
     return KNNG_OK;
 }
+
+#include "dist_api.cuh"
 
 }  // namespace
 
@@ -940,6 +954,85 @@ knng_status knng_merge(const void* vecA, int64_t nA, const uint32_t* idsA, const
     R.export_graph(out_ids, out_dists);
     R.collect_stats(merge_iters);
     return c.finish();
+}
+
+// ------------------------------------------------------------ multi-GPU
+knng_status knng_get_unique_id(void* host_out128) {
+    if (!host_out128) return fail(KNNG_E_USAGE, "null pointer argument");
+    NcclApi& A = NcclApi::get();
+    if (!A.ok()) return fail(KNNG_E_NCCL, "%s", A.error.c_str());
+    ncclUniqueId id;
+    const ncclResult_t r = A.GetUniqueId(&id);
+    if (r != ncclSuccess) return fail(KNNG_E_NCCL, "ncclGetUniqueId: %s", A.GetErrorString(r));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    memcpy(host_out128, &id, sizeof(id));
+    return KNNG_OK;
+}
+
+knng_status knng_comm_init(int32_t rank, int32_t world, const void* host_id128, void** comm) {
+    if (!host_id128 || !comm) return fail(KNNG_E_USAGE, "null pointer argument");
+    if (world < 1 || rank < 0 || rank >= world) return fail(KNNG_E_USAGE, "rank must be in [0, world)");
+    NcclApi& A = NcclApi::get();
+    if (!A.ok()) return fail(KNNG_E_NCCL, "%s", A.error.c_str());
+    ncclUniqueId id;
+    memcpy(&id, host_id128, sizeof(id));
+    auto* c = new NcclComm();
+    c->rank = rank;
+    c->world = world;
+    const ncclResult_t r = A.CommInitRank(&c->comm, world, id, rank);
+    if (r != ncclSuccess) {
+        c->comm = nullptr;
+        delete c;
+        return fail(KNNG_E_NCCL, "ncclCommInitRank: %s", A.GetErrorString(r));
+    }
+    *comm = static_cast<Comm*>(c);
+    return KNNG_OK;
+}
+
+knng_status knng_comm_init_local(int32_t world, void** host_comms) {
+    if (!host_comms || world < 1) return fail(KNNG_E_USAGE, "bad arguments");
+    auto hub = std::make_shared<Hub>(world);
+    for (int r = 0; r < world; ++r) {
+        auto* c = new LocalComm();
+        c->rank = r;
+        c->world = world;
+        c->hub = hub;
+        host_comms[r] = static_cast<Comm*>(c);
+    }
+    return KNNG_OK;
+}
+
+knng_status knng_comm_destroy(void* comm) {
+    delete static_cast<Comm*>(comm);
+    return KNNG_OK;
+}
+
+knng_status knng_build_sharded(void* comm, const void* local_vectors, int64_t n_local, int64_t global_offset,
+                               int64_t n_total, knng_dtype dt, int32_t d, int32_t k, knng_metric metric,
+                               int32_t iters, int32_t merge_iters, const int32_t* host_level_iters,
+                               int32_t sample_size, uint64_t seed, uint32_t* out_ids_local,
+                               float* out_dists_local, void* stream) {
+    if (!comm) return fail(KNNG_E_USAGE, "null communicator");
+    Comm& C = *static_cast<Comm*>(comm);
+    knng_status s = check_common(dt, n_local, d, k, metric, sample_size);
+    if (s) return s;
+    if (C.world & (C.world - 1)) return fail(KNNG_E_USAGE, "the world size must be a power of two");
+    if (n_total != n_local * C.world) return fail(KNNG_E_USAGE, "n_total must be world * n_local (equal shards)");
+    if (global_offset != static_cast<int64_t>(C.rank) * n_local)
+        return fail(KNNG_E_USAGE, "global_offset must be rank * n_local");
+    if (n_total >= 0xFFFFFFFFll) return fail(KNNG_E_USAGE, "n_total must be < 2^32 - 1");
+    if (iters < 1 || iters > kMaxIters) return fail(KNNG_E_USAGE, "iters must be in [1, %d]", kMaxIters);
+    int levels = 0;
+    while ((1 << levels) < C.world) ++levels;
+    for (int l = 0; l < levels; ++l) {
+        const int mi = host_level_iters ? host_level_iters[l] : merge_iters;
+        if (mi < 0 || mi > kMaxIters) return fail(KNNG_E_USAGE, "merge iterations must be in [0, %d]", kMaxIters);
+    }
+    if (!is_device_ptr(local_vectors) || !is_device_ptr(out_ids_local) || !is_device_ptr(out_dists_local))
+        return fail(KNNG_E_USAGE, "vectors and outputs must be device pointers");
+    return run_sharded(C, local_vectors, n_local, global_offset, n_total, dt, d, k, metric, iters, merge_iters,
+                       host_level_iters, sample_size, seed, out_ids_local, out_dists_local,
+                       static_cast<cudaStream_t>(stream));
 }
 
 // ------------------------------------------------------------ introspection

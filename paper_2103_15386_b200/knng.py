@@ -50,6 +50,11 @@ SIGNATURES = [
     ("knng_build_host", i32, [P, i32, i64, i32, i32, i32, i32, i32, u64, P, P, P]),
     ("knng_merge_workspace_bytes", sz, [i32, i64, i64, i32, i32, i32, i32]),
     ("knng_merge", i32, [P, i64, P, P, P, i64, P, P, i32, i32, i32, i32, i32, i32, i32, u64, P, P, P, sz, P]),
+    ("knng_get_unique_id", i32, [P]),
+    ("knng_comm_init", i32, [i32, i32, P, P]),
+    ("knng_comm_init_local", i32, [i32, P]),
+    ("knng_comm_destroy", i32, [P]),
+    ("knng_build_sharded", i32, [P, P, i64, i64, i64, i32, i32, i32, i32, i32, i32, P, i32, u64, P, P, P]),
     ("knng_bruteforce", i32, [P, i32, i64, i32, i32, P, i64, i32, P, P, P]),
     ("knng_debug_init", i32, [P, i32, i64, i32, i32, i32, u64, P, P, P]),
     ("knng_debug_iterate", i32, [P, i32, i64, i32, i32, i32, i32, u32, u64, i64, P, P, P, P, sz, P]),
@@ -188,6 +193,58 @@ def knng_merge(vecA, idsA, distsA, vecB, idsB, distsB, k: int, merge_iters: int,
     _check(lib().knng_merge(_ptr(vecA), nA, _ptr(idsA), _ptr(distsA), _ptr(vecB), nB, _ptr(idsB),
                             _ptr(distsB), dt, d, k, _metric(metric), merge_iters, sample_size, level, seed,
                             _ptr(out_ids), _ptr(out_dists), ws_ptr, ws_bytes, _stream(stream)))
+    return out_ids, out_dists
+
+
+# ------------------------------------------------------------------ multi-GPU
+def knng_get_unique_id() -> bytes:
+    """NCCL unique id (128 bytes) for knng_comm_init; rank 0 creates it."""
+    buf = C.create_string_buffer(128)
+    _check(lib().knng_get_unique_id(buf))
+    return buf.raw
+
+
+def knng_comm_init(rank: int, world: int, uid: bytes) -> int:
+    """NCCL communicator handle of this rank (the current CUDA device)."""
+    assert len(uid) == 128
+    h = C.c_void_p()
+    _check(lib().knng_comm_init(rank, world, C.create_string_buffer(uid, 128), C.byref(h)))
+    return h.value
+
+
+def knng_comm_init_local(world: int) -> list[int]:
+    """`world` in-process communicators (one per host thread)."""
+    arr = (C.c_void_p * world)()
+    _check(lib().knng_comm_init_local(world, arr))
+    return [arr[i] for i in range(world)]
+
+
+def knng_comm_destroy(comm: int):
+    _check(lib().knng_comm_destroy(comm))
+
+
+def knng_build_sharded(comm: int, rank: int, world: int, local_vectors, k: int, iters: int, merge_iters,
+                       sample_size: int, seed: int = 0, metric="l2", out_ids=None, out_dists=None, stream=None):
+    """Collective GNND + log-depth GGM tree (include/knng.h): this rank's rows
+    [rank n_local, (rank+1) n_local) -> their lists with global ids.
+    merge_iters: one count, or one per tree level."""
+    import torch
+    assert local_vectors.is_cuda and local_vectors.is_contiguous() and local_vectors.dim() == 2
+    nl, d = local_vectors.shape
+    if out_ids is None:
+        out_ids = torch.empty((nl, k), dtype=torch.int32, device=local_vectors.device)
+    if out_dists is None:
+        out_dists = torch.empty((nl, k), dtype=torch.float32, device=local_vectors.device)
+    levels = max(0, world.bit_length() - 1)
+    if isinstance(merge_iters, int):
+        lv, mi = None, merge_iters
+    else:
+        its = [int(x) for x in merge_iters]
+        its = (its + its[-1:] * levels)[:max(levels, 1)]
+        lv, mi = (C.c_int32 * len(its))(*its), its[0]
+    _check(lib().knng_build_sharded(comm, _ptr(local_vectors), nl, rank * nl, world * nl, _dtype_code(local_vectors),
+                                    d, k, _metric(metric), iters, mi, lv, sample_size, seed, _ptr(out_ids),
+                                    _ptr(out_dists), _stream(stream)))
     return out_ids, out_dists
 
 
