@@ -265,7 +265,7 @@ def main():
     import torch.distributed as dist
 
     import paper_2103_15386_b200.knng as K
-    from paper_2103_15386_b200.sharded import CudaOps, knng_build_sharded
+    from paper_2103_15386_b200.sharded import CudaOps, knng_build_sharded_nccl, nccl_comm
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -280,6 +280,7 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
+        nccl_comm()  # libknng's own NCCL communicator (unique id broadcast by torch)
     coll_dev = "cuda" if backend == "nccl" else "cpu"
 
     def barrier():
@@ -334,9 +335,10 @@ def main():
         if world == 1:
             K.knng_build(Xd, args.k, args.iters, args.p, args.seed, "l2", ids, dists, ws, stream)
             ops.history.extend(K.knng_last_stats())
-        else:  # one shard per GPU, log-depth GGM tree over NCCL (sharded.py)
-            out["g"] = knng_build_sharded(Xd, world, args.k, args.iters, level_iters, args.p, args.seed,
-                                          ops=ops)
+        else:  # one shard per GPU; every tree level merged by all GPUs of its group (C ABI, NCCL)
+            out["g"] = knng_build_sharded_nccl(Xd, args.k, args.iters, level_iters, args.p, args.seed,
+                                               stream=stream)
+            ops.history.extend(K.knng_last_stats())
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -393,8 +395,8 @@ def main():
                     raise RuntimeError(K.knng_last_error())
             else:
                 Xd.copy_(Xh, non_blocking=True)
-                gi, gd = knng_build_sharded(Xd, world, args.k, args.iters, level_iters, args.p, args.seed,
-                                            ops=CudaOps(stream=stream))
+                gi, gd = knng_build_sharded_nccl(Xd, args.k, args.iters, level_iters, args.p, args.seed,
+                                                 stream=stream)
                 ih.copy_(gi, non_blocking=True)
                 dh.copy_(gd, non_blocking=True)
                 torch.cuda.synchronize()
@@ -410,7 +412,7 @@ def main():
         barrier()
         e2e = {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(X.nbytes),
                "d2h_bytes_per_step": int(n * args.k * 8),
-               "api": "knng_build_host" if world == 1 else "knng_build_sharded (per-rank H2D/D2H)"}
+               "api": "knng_build_host" if world == 1 else "knng_build_sharded over NCCL (per-rank H2D/D2H)"}
 
     # ---- roofline of the dominant kernel (k_join), DESIGN.md section 6:
     # HBM view: algorithmic gather bytes = rows x (d x element + 4 id bytes);
@@ -466,7 +468,8 @@ def main():
                    "l2_flush": "inputs (512 MB) larger than L2"}
         else:
             cfg = {"workload": f"sharded SIFT-shaped {world} x {n} (one {n}-row shard per GPU, GNND per shard + "
-                               f"log-depth GGM tree over NCCL: the C4/C5 scheme at C2 shard size)",
+                               f"log-depth GGM tree, every level merged by all GPUs of its group with records "
+                               f"exchanged over NCCL (knng_build_sharded): the C4/C5 scheme at C2 shard size)",
                    "n": world * n, "n_per_gpu": n,
                    "d": d, "k": args.k, "sample_size": args.p, "iters": args.iters,
                    "merge_iters": level_iters, "shards": world, "metric": "l2",

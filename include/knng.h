@@ -126,6 +126,23 @@ knng_status knng_merge(const void* vecA, int64_t nA, const uint32_t* idsA,
                        size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------------------------
+ * knng_extend -- incremental construction ("As the new data come in,
+ * GNND is called to build a sub-graph on the first hand.  Thereafter, GGM is
+ * called to join this new sub-graph into the existing k-NN graph").
+ * = knng_build(vec_new, seed) followed by knng_merge(existing graph = A,
+ * batch graph = B, merge_iters, level 0, seed).
+ *   vec_old [n_old][d], ids_old/dists_old [n_old][k]: the existing graph
+ *   (ids < n_old); vec_new [n_new][d]: the batch (its rows get the ids
+ *   n_old .. n_old + n_new - 1).  out_ids/out_dists [(n_old + n_new)][k].
+ *   All device.  Errors as knng_build / knng_merge.  knng_last_stats: the
+ *   batch build's iterations, then the merge's.
+ * ---------------------------------------------------------------------- */
+knng_status knng_extend(const void* vec_old, int64_t n_old, const uint32_t* ids_old, const float* dists_old,
+                        const void* vec_new, int64_t n_new, knng_dtype dt, int32_t d, int32_t k,
+                        knng_metric metric, int32_t iters, int32_t merge_iters, int32_t sample_size,
+                        uint64_t seed, uint32_t* out_ids, float* out_dists, void* stream);
+
+/* ------------------------------------------------------------------------
  * Multi-GPU (one process -- or one host thread -- per GPU).
  * The paper builds sub-graphs of the shards on different GPUs and merges
  * them with GGM ("GGM allows the k-NN graph to be built on multiple

@@ -273,3 +273,13 @@ def tree_build(X, shards, k, p, iters, merge_iters, seed, metric=L2SQ):
         width *= 2
         level += 1
     return keys
+
+
+def extend(X_old, keys_old, X_new, k, p, iters, merge_iters, seed, metric=L2SQ):
+    """Incremental construction: GNND on the new batch (seed), then
+    GGM of the existing graph (A, ids < n_old) with the batch graph (B, ids
+    re-based by n_old), level 0, the same seed.  Returns keys [n_old + n_new, k]."""
+    n_old = X_old.shape[0]
+    ids, dists = build(X_new, k, p, iters, seed, metric)
+    keys_in = np.concatenate([keys_old, key(dists, ids.astype(np.uint64) + np.uint64(n_old))])
+    return merge(np.concatenate([X_old, X_new]), keys_in, n_old, k, p, merge_iters, seed, 0, metric)

@@ -956,6 +956,46 @@ knng_status knng_merge(const void* vecA, int64_t nA, const uint32_t* idsA, const
     return c.finish();
 }
 
+// ------------------------------------------------------------ incremental
+knng_status knng_extend(const void* vec_old, int64_t n_old, const uint32_t* ids_old, const float* dists_old,
+                        const void* vec_new, int64_t n_new, knng_dtype dt, int32_t d, int32_t k, knng_metric metric,
+                        int32_t iters, int32_t merge_iters, int32_t sample_size, uint64_t seed, uint32_t* out_ids,
+                        float* out_dists, void* stream) {
+    // "As the new data come in, GNND is called to build a sub-graph on the
+    // first hand.  Thereafter, GGM is called to join this new sub-graph into
+    // the existing k-NN graph": knng_build on the batch, knng_merge.
+    knng_status s = check_common(dt, n_new, d, k, metric, sample_size);
+    if (s) return s;
+    if ((s = check_common(dt, n_old + n_new, d, k, metric, sample_size))) return s;
+    if (n_old <= k) return fail(KNNG_E_USAGE, "the existing graph needs n_old > k");
+    if (iters < 1 || iters > kMaxIters) return fail(KNNG_E_USAGE, "iters must be in [1, %d]", kMaxIters);
+    if (!is_device_ptr(vec_new) || !is_device_ptr(out_ids) || !is_device_ptr(out_dists))
+        return fail(KNNG_E_USAGE, "arguments must be device pointers");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    void *ib = nullptr, *db = nullptr;
+    const size_t gb = static_cast<size_t>(n_new) * k * 4;
+    if (cudaMallocAsync(&ib, gb, st) != cudaSuccess || cudaMallocAsync(&db, gb, st) != cudaSuccess) {
+        cudaGetLastError();
+        if (ib) cudaFreeAsync(ib, st);
+        return fail(KNNG_E_NOMEM, "cannot allocate the batch graph");
+    }
+    std::vector<knng_iter_stats> hist;
+    s = knng_build(vec_new, dt, n_new, d, k, metric, iters, sample_size, seed, static_cast<uint32_t*>(ib),
+                   static_cast<float*>(db), nullptr, 0, stream);
+    if (s == KNNG_OK) {
+        hist = g_last_stats;
+        s = knng_merge(vec_old, n_old, ids_old, dists_old, vec_new, n_new, static_cast<const uint32_t*>(ib),
+                       static_cast<const float*>(db), dt, d, k, metric, merge_iters, sample_size, 0, seed, out_ids,
+                       out_dists, nullptr, 0, stream);
+        if (s == KNNG_OK) hist.insert(hist.end(), g_last_stats.begin(), g_last_stats.end());
+    }
+    cudaFreeAsync(ib, st);
+    cudaFreeAsync(db, st);
+    cudaStreamSynchronize(st);
+    if (s == KNNG_OK) g_last_stats = hist;
+    return s;
+}
+
 // ------------------------------------------------------------ multi-GPU
 knng_status knng_get_unique_id(void* host_out128) {
     if (!host_out128) return fail(KNNG_E_USAGE, "null pointer argument");

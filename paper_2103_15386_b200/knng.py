@@ -50,6 +50,7 @@ SIGNATURES = [
     ("knng_build_host", i32, [P, i32, i64, i32, i32, i32, i32, i32, u64, P, P, P]),
     ("knng_merge_workspace_bytes", sz, [i32, i64, i64, i32, i32, i32, i32]),
     ("knng_merge", i32, [P, i64, P, P, P, i64, P, P, i32, i32, i32, i32, i32, i32, i32, u64, P, P, P, sz, P]),
+    ("knng_extend", i32, [P, i64, P, P, P, i64, i32, i32, i32, i32, i32, i32, i32, u64, P, P, P]),
     ("knng_get_unique_id", i32, [P]),
     ("knng_comm_init", i32, [i32, i32, P, P]),
     ("knng_comm_init_local", i32, [i32, P]),
@@ -193,6 +194,28 @@ def knng_merge(vecA, idsA, distsA, vecB, idsB, distsB, k: int, merge_iters: int,
     _check(lib().knng_merge(_ptr(vecA), nA, _ptr(idsA), _ptr(distsA), _ptr(vecB), nB, _ptr(idsB),
                             _ptr(distsB), dt, d, k, _metric(metric), merge_iters, sample_size, level, seed,
                             _ptr(out_ids), _ptr(out_dists), ws_ptr, ws_bytes, _stream(stream)))
+    return out_ids, out_dists
+
+
+def knng_extend(vec_old, ids_old, dists_old, vec_new, k: int, iters: int, merge_iters: int, sample_size: int,
+                seed: int = 0, metric="l2", stream=None):
+    """Incremental construction: GNND on the batch, GGM into the
+    existing graph.  Returns (ids, dists) [n_old + n_new, k]."""
+    import torch
+    n_old, d = vec_old.shape
+    n_new = vec_new.shape[0]
+    if vec_new.dim() != 2 or vec_new.shape[1] != d or vec_new.dtype != vec_old.dtype:
+        raise ValueError("vec_new must match vec_old's width and dtype")
+    if tuple(ids_old.shape) != (n_old, k) or tuple(dists_old.shape) != (n_old, k):
+        raise ValueError(f"ids_old/dists_old must be [{n_old}, {k}]")
+    for t in (vec_old, ids_old, dists_old, vec_new):
+        if not (t.is_cuda and t.is_contiguous()):
+            raise ValueError("knng_extend needs contiguous CUDA tensors")
+    out_ids = torch.empty((n_old + n_new, k), dtype=torch.int32, device=vec_old.device)
+    out_dists = torch.empty((n_old + n_new, k), dtype=torch.float32, device=vec_old.device)
+    _check(lib().knng_extend(_ptr(vec_old), n_old, _ptr(ids_old), _ptr(dists_old), _ptr(vec_new), n_new,
+                             _dtype_code(vec_old), d, k, _metric(metric), iters, merge_iters, sample_size, seed,
+                             _ptr(out_ids), _ptr(out_dists), _stream(stream)))
     return out_ids, out_dists
 
 

@@ -1,5 +1,15 @@
 """Sharded GNND build: divide and conquer over GPUs with a log-depth GGM tree.
 
+Two entry points:
+  * knng_build_sharded_nccl -- the product multi-GPU path: the C ABI's
+    knng_build_sharded (every tree level merged by all GPUs of its group,
+    records exchanged over NCCL inside libknng.so, SURVEY.md 8(e) stage B).
+    torch.distributed only broadcasts the NCCL unique id (nccl_comm).
+  * knng_build_sharded -- stage A host plumbing below: per-level block
+    transfers with torch.distributed send/recv and one knng_merge per group
+    on its leader.  It runs over any backend (gloo on CPU in the tests, with
+    the oracle injected as compute) and is kept as the staged fallback.
+
 The paper's out-of-memory scheme (Sec. 4.2): the set is split into
 shards, "sub-graphs are constructed by GNND ... on different GPUs",
 then the sub-graphs are joined by the GPU graph merge GGM (Alg. 3).
@@ -215,3 +225,36 @@ def _build_sharded(local_vectors, shards, k, iters, merge_iters, sample_size, se
     comm.recv_into(ids, 0)
     comm.recv_into(dists, 0)
     return ids, dists
+
+
+# ---------------------------------------------------------------- stage B (C ABI)
+_COMMS = {}
+
+
+def nccl_comm(group=None):
+    """The libknng NCCL communicator of this rank for `group` (cached): rank 0
+    creates the unique id, torch.distributed broadcasts it (the only role of
+    torch here), every rank calls knng_comm_init on its current device."""
+    import torch.distributed as dist
+
+    from . import knng as K
+    key = id(group)
+    if key in _COMMS:
+        return _COMMS[key]
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    obj = [K.knng_get_unique_id() if rank == 0 else None]
+    src = dist.get_global_rank(group, 0) if group is not None else 0
+    dist.broadcast_object_list(obj, src=src, group=group)
+    comm = (K.knng_comm_init(rank, world, obj[0]), rank, world)
+    _COMMS[key] = comm
+    return comm
+
+
+def knng_build_sharded_nccl(local_vectors, k: int, iters: int, merge_iters, sample_size: int, seed: int = 0,
+                            metric="l2", group=None, stream=None):
+    """Collective build over the ranks of `group` (one GPU each): this rank's
+    rows [rank n_local, (rank+1) n_local) -> their lists, global ids."""
+    from . import knng as K
+    comm, rank, world = nccl_comm(group)
+    return K.knng_build_sharded(comm, rank, world, local_vectors, k, iters, merge_iters, sample_size, seed, metric,
+                                stream=stream)

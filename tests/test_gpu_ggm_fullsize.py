@@ -172,3 +172,19 @@ def test_fullsize_ggm_2x500k_restricted_iteration_sampled_targets(K, c2):
     for t in targets[:500]:
         fresh = set(orc.key_ids(gk[t]).tolist()) - set(orc.key_ids(keys[t]).tolist())
         assert all((v >= h) != (t >= h) for v in fresh)
+
+
+@pytest.mark.parametrize("shape,dtype,metric", [("c1", "f32", "l2"), ("sift", "u8", "l2"), ("deep", "f32", "cosine")])
+def test_extend_equals_oracle(K, shape, dtype, metric):
+    # knng_extend = GNND on the batch + GGM into the existing graph
+    m = orc.COSINE if metric == "cosine" else orc.L2SQ
+    n_old, n_new, k, p = 2500, 1500, 16, 8
+    X = (datagen.make("sift", n_old + n_new, seed=31, dtype=dtype) if shape == "sift"
+         else datagen.make(shape, n_old + n_new, seed=31, d=32 if shape == "c1" else 96))
+    oi, od = orc.build(X[:n_old], k, p, 5, 4, m)
+    expect = orc.extend(X[:n_old], orc.key(od, oi), X[n_old:], k, p, 5, 4, 8, m)
+    gi, gd = K.knng_extend(dev(X[:n_old]), dev(oi.view(np.int32)), dev(od), dev(X[n_old:]), k, 5, 4, p, seed=8,
+                           metric=metric)
+    assert np.array_equal(gi.cpu().numpy().view(np.uint32), orc.key_ids(expect))
+    assert np.array_equal(gd.cpu().numpy(), orc.key_dists(expect))
+    assert len(K.knng_last_stats()) == 5 + 4

@@ -172,3 +172,21 @@ def test_phi_spec_examples():
     gt = orc.bruteforce(X, np.arange(500), 8)
     keys, _ = orc.init(X, 8, 1)
     assert orc.phi(gt) <= orc.phi(keys)
+
+
+def test_incremental_extension_quality():
+    # P:296 incremental construction: a 6k graph extended by a 4k batch
+    # (GNND on the batch + GGM) stays within 0.05 recall@10 of the direct
+    # build of all 10k rows, and its lists keep the invariants.
+    X = datagen.make("c1", 10000, seed=10)
+    q = datagen.sample_nodes(10000, 1000)
+    gt = orc.bruteforce(X, q, 10)
+    k, p = 10, 8
+    ids, dists = orc.build(X, k, p, 10, 2)
+    direct = orc.recall(orc.key(dists, ids)[q], gt, 10)
+    oi, od = orc.build(X[:6000], k, p, 10, 2)
+    keys = orc.extend(X[:6000], orc.key(od, oi), X[6000:], k, p, 10, 6, 3)
+    assert keys.shape == (10000, k)
+    assert orc.recall(keys[q], gt, 10) >= direct - 0.05
+    assert (keys[:, 1:] > keys[:, :-1]).all()
+    assert (orc.key_ids(keys) != np.arange(10000)[:, None]).all()

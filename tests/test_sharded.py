@@ -179,3 +179,68 @@ def test_sharded_per_level_merge_iters():
                                     [CASE["merge_iters"]] * 2, CASE["p"], CASE["seed"], ops=OracleOps())
     _, expect = _expected()
     assert np.array_equal(orc.key(dists.numpy(), ids.numpy().view(np.uint32)), expect)
+
+
+# ------------------------------------------------------------------ stage B plumbing (CPU, gloo)
+def _uid_worker(rank, world, port, out_dir):
+    import torch.distributed as dist
+
+    import paper_2103_15386_b200.knng as K
+    from paper_2103_15386_b200 import sharded
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # the unique-id broadcast of nccl_comm, without the GPU-side init
+        obj = [K.knng_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        with open(os.path.join(out_dir, f"uid{rank}.bin"), "wb") as f:
+            f.write(obj[0])
+        assert sharded._COMMS == {}
+    finally:
+        dist.destroy_process_group()
+
+
+def test_stage_b_unique_id_broadcast_gloo_world2(tmp_path):
+    """knng_build_sharded_nccl's rendezvous (torch provides
+    only the ncclUniqueId broadcast): rank 0's 128-byte NCCL id from
+    libknng.so reaches every rank of a world-size-2 gloo group intact."""
+    import paper_2103_15386_b200.knng as K
+    try:
+        K.knng_get_unique_id()
+    except K.KnngError as e:  # no NCCL on this host: nothing to broadcast
+        pytest.skip(str(e))
+    import torch.multiprocessing as mp
+    mp.spawn(_uid_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    a = (tmp_path / "uid0.bin").read_bytes()
+    b = (tmp_path / "uid1.bin").read_bytes()
+    assert len(a) == 128 and a == b and any(a)
+
+
+def test_build_sharded_abi_validation_without_gpu():
+    """Host-side checks of knng_build_sharded run before any CUDA call."""
+    import ctypes as C
+
+    import paper_2103_15386_b200.knng as K
+    L = K.lib()
+    comms = K.knng_comm_init_local(2)
+    try:
+        ok = dict(n_local=100, goff=0, ntot=200, k=10, iters=3, mi=2, p=5)
+
+        def call(comm, **kw):
+            a = dict(ok, **kw)
+            return L.knng_build_sharded(comm, None, a["n_local"], a["goff"], a["ntot"], K.KNNG_F32, 8, a["k"],
+                                        K.KNNG_L2SQ, a["iters"], a["mi"], None, a["p"], 1, None, None, None)
+        assert call(comms[0], ntot=300) == K.KNNG_E_USAGE          # unequal shards
+        assert call(comms[1], goff=0) == K.KNNG_E_USAGE            # rank 1 must start at n_local
+        assert call(comms[0], p=10) == K.KNNG_E_USAGE              # p < k
+        assert call(comms[0], mi=-1) == K.KNNG_E_USAGE
+        assert call(None) == K.KNNG_E_USAGE
+        three = (C.c_void_p * 3)()
+        assert L.knng_comm_init_local(3, three) == K.KNNG_OK
+        assert L.knng_build_sharded(three[0], None, 100, 0, 300, 0, 8, 10, 0, 3, 2, None, 5, 1, None, None,
+                                    None) == K.KNNG_E_USAGE  # world not a power of two
+        for h in three:
+            K.knng_comm_destroy(h)
+    finally:
+        for c in comms:
+            K.knng_comm_destroy(c)
