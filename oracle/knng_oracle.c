@@ -70,7 +70,13 @@ static int ds_open(dataset* ds, const void* X, int dtype, int64_t n, int d,
     ds->X = X; ds->dtype = dtype; ds->n = n; ds->d = d; ds->metric = metric;
     ds->Xn = NULL;
     if (dtype != ORC_F32 && dtype != ORC_U8) return ORC_E_USAGE;
-    if (metric != ORC_L2SQ && metric != ORC_COSINE) return ORC_E_USAGE;
+    if (metric != ORC_L2SQ && metric != ORC_COSINE && metric != ORC_CHI2) return ORC_E_USAGE;
+    if (metric == ORC_CHI2 && dtype == ORC_F32) {
+        /* chi-square needs non-negative components (D39) */
+        const float* F = (const float*)X;
+        for (int64_t i = 0; i < n * (int64_t)d; ++i)
+            if (!(F[i] >= 0.0f)) return ORC_E_DOMAIN;
+    }
     if (metric == ORC_COSINE) {
         if (dtype != ORC_F32) return ORC_E_USAGE;
         const float* F = (const float*)X;
@@ -90,8 +96,30 @@ static int ds_open(dataset* ds, const void* X, int dtype, int64_t n, int d,
 
 static void ds_close(dataset* ds) { free(ds->Xn); ds->Xn = NULL; }
 
+/* chi-square ("K-Square"), D39: terms (x_i - y_i)^2 / (x_i + y_i) in
+ * dimension order; q = t / s (0 when s = 0), acc = fmaf(q, t, acc). */
+static float chi2_term(float x, float y, float acc) {
+    float t = x - y;
+    float s = x + y;
+    float q = (s > 0.0f) ? t / s : 0.0f;
+    return fmaf(q, t, acc);
+}
+
 static float ds_dist(const dataset* ds, int64_t a, int64_t b) {
     const int d = ds->d;
+    if (ds->metric == ORC_CHI2) {
+        float acc = 0.0f;
+        if (ds->dtype == ORC_U8) {
+            const uint8_t* x = (const uint8_t*)ds->X + (size_t)a * d;
+            const uint8_t* y = (const uint8_t*)ds->X + (size_t)b * d;
+            for (int i = 0; i < d; ++i) acc = chi2_term((float)x[i], (float)y[i], acc);
+        } else {
+            const float* x = (const float*)ds->X + (size_t)a * d;
+            const float* y = (const float*)ds->X + (size_t)b * d;
+            for (int i = 0; i < d; ++i) acc = chi2_term(x[i], y[i], acc);
+        }
+        return acc;
+    }
     if (ds->metric == ORC_COSINE) {
         const float* x = ds->Xn + (size_t)a * d;
         const float* y = ds->Xn + (size_t)b * d;
@@ -130,6 +158,33 @@ float orc_distance(const void* X, int dtype, int64_t n, int d, int metric,
 }
 
 /* ------------------------------------------------------------------ */
+/* Process-wide oracle options (test infrastructure)                    */
+/* ------------------------------------------------------------------ */
+static int g_update_mode = ORC_UPDATE_SELECTIVE;
+static int g_seg_size = 32;
+
+int orc_set_option(const char* name, int value) {
+    if (strcmp(name, "update") == 0) {
+        if (value != ORC_UPDATE_SELECTIVE && value != ORC_UPDATE_FULL) return ORC_E_USAGE;
+        g_update_mode = value;
+        return ORC_OK;
+    }
+    if (strcmp(name, "segment_size") == 0) {
+        if (value < 1) return ORC_E_USAGE;
+        g_seg_size = value;
+        return ORC_OK;
+    }
+    return ORC_E_USAGE;
+}
+
+/* segments of a k-list ("divided into k / 32 segments", D18/D40):
+ * s = k / seg for k >= 2 seg (k a multiple of seg), else 1 */
+int orc_segments(int k) {
+    if (k >= 2 * g_seg_size) return (k % g_seg_size == 0) ? k / g_seg_size : -1;
+    return 1;
+}
+
+/* ------------------------------------------------------------------ */
 /* Bounded sorted k-NN list (D16)                          */
 /* ------------------------------------------------------------------ */
 static int list_has_id(const uint64_t* L, int k, uint32_t id) {
@@ -140,7 +195,31 @@ static int list_has_id(const uint64_t* L, int k, uint32_t id) {
 
 /* InsertIntoNNList(G[u], v, d): accept iff key < current maximum and id not
  * already in the list; the farthest entry is evicted; the new entry is NEW.
- * Returns 1 if inserted. */
+ * Returns 1 if inserted.
+ * Segmented list (s > 1, D40): the list is kept as the sorted union
+ * of its s segments; entry id v belongs to segment v % s, every segment
+ * holds k / s entries.  The candidate competes only with its own segment:
+ * accept iff key < that segment's maximum and v is not in the list (it
+ * could only be in its own segment); that segment's maximum is evicted. */
+static int list_insert_seg(uint64_t* L, uint8_t* F, int k, int s, uint64_t key) {
+    if (list_has_id(L, k, KEY_ID(key))) return 0;
+    const uint32_t g = KEY_ID(key) % (uint32_t)s;
+    int evict = -1; /* position of the segment's maximum (segments are full) */
+    for (int j = k - 1; j >= 0; --j)
+        if (L[j] != ORC_SENTINEL && KEY_ID(L[j]) % (uint32_t)s == g) { evict = j; break; }
+    if (evict < 0 || !(key < L[evict])) return 0;
+    for (int j = evict; j < k - 1; ++j) { L[j] = L[j + 1]; F[j] = F[j + 1]; } /* remove it */
+    int pos = k - 1;
+    while (pos > 0 && L[pos - 1] > key) {
+        L[pos] = L[pos - 1];
+        F[pos] = F[pos - 1];
+        --pos;
+    }
+    L[pos] = key;
+    F[pos] = 1;
+    return 1;
+}
+
 static int list_insert(uint64_t* L, uint8_t* F, int k, uint64_t key) {
     if (!(key < L[k - 1])) return 0;
     if (list_has_id(L, k, KEY_ID(key))) return 0;
@@ -157,6 +236,11 @@ static int list_insert(uint64_t* L, uint8_t* F, int k, uint64_t key) {
 
 int orc_list_insert(uint64_t* list, uint8_t* flags, int k, uint64_t key) {
     return list_insert(list, flags, k, key);
+}
+
+int orc_list_insert_seg(uint64_t* list, uint8_t* flags, int k, int s, uint64_t key) {
+    if (s < 1 || k % s) return -1;
+    return list_insert_seg(list, flags, k, s, key);
 }
 
 void orc_pair_index(int64_t t, int64_t* u, int64_t* v) {
@@ -188,19 +272,29 @@ static void sort_keys_flags(uint64_t* L, uint8_t* F, int k) {
 static int init_list(const dataset* ds, int k, uint64_t seed, int64_t s,
                      uint64_t* L, uint8_t* F) {
     int64_t n = ds->n;
+    const int nseg = orc_segments(k), per = k / nseg;
     uint32_t* chosen = (uint32_t*)malloc((size_t)k * sizeof(uint32_t));
     if (!chosen) return ORC_E_NOMEM;
     int cnt = 0;
-    for (uint32_t j = 0; cnt < k; ++j) {
-        uint32_t out[4];
-        philox_words(ORC_TAG_INIT, (uint32_t)s, j, (uint32_t)((uint64_t)s >> 32),
-                     seed, out);
-        uint64_t r = orc_uniform(out, (uint64_t)(n - 1));
-        uint32_t v = (uint32_t)(r + (r >= (uint64_t)s ? 1 : 0));
-        int dup = 0;
-        for (int i = 0; i < cnt; ++i)
-            if (chosen[i] == v) { dup = 1; break; }
-        if (!dup) chosen[cnt++] = v;
+    /* segment g (residue g mod nseg; one segment: all ids): per distinct
+     * ids != s, drawn in counter order j from Philox(INIT, s, j | g << 24,
+     * s >> 32) over the residue class without s (D2, D40) */
+    for (int g = 0; g < nseg; ++g) {
+        const int64_t M = (n - g + nseg - 1) / nseg;         /* ids = g mod nseg */
+        const int self_in = (s % nseg) == g;
+        const int start = cnt;
+        for (uint32_t j = 0; cnt < start + per; ++j) {
+            uint32_t out[4];
+            philox_words(ORC_TAG_INIT, (uint32_t)s, j | ((uint32_t)g << 24),
+                         (uint32_t)((uint64_t)s >> 32), seed, out);
+            uint64_t r = orc_uniform(out, (uint64_t)(M - self_in));
+            uint64_t v = (uint64_t)g + (uint64_t)nseg * r;
+            if (self_in && v >= (uint64_t)s) v += (uint64_t)nseg;
+            int dup = 0;
+            for (int i = start; i < cnt; ++i)
+                if (chosen[i] == (uint32_t)v) { dup = 1; break; }
+            if (!dup) chosen[cnt++] = (uint32_t)v;
+        }
     }
     for (int i = 0; i < k; ++i) {
         L[i] = KEY(ds_dist(ds, s, chosen[i]), chosen[i]);
@@ -214,6 +308,8 @@ static int init_list(const dataset* ds, int k, uint64_t seed, int64_t s,
 int orc_init(const void* X, int dtype, int64_t n, int d, int metric, int k,
              uint64_t seed, uint64_t* keys, uint8_t* flags) {
     if (k < 1 || n <= k || d < 1) return ORC_E_USAGE;
+    const int nseg = orc_segments(k);
+    if (nseg < 1 || (nseg > 1 && n < (int64_t)k + nseg)) return ORC_E_USAGE;
     dataset ds;
     int rc = ds_open(&ds, X, dtype, n, d, metric);
     if (rc) return rc;
@@ -378,7 +474,11 @@ static void offer(uint64_t* keys, uint8_t* flags, int k, const uint8_t* tmask,
     if (cand == ORC_SENTINEL) return; /* D15: (inf, inf) inserts nothing */
     st->candidates++;
     if (tmask && !tmask[target]) return;
-    list_insert(keys + (size_t)target * k, flags + (size_t)target * k, k, cand);
+    const int nseg = orc_segments(k);
+    if (nseg > 1)
+        list_insert_seg(keys + (size_t)target * k, flags + (size_t)target * k, k, nseg, cand);
+    else
+        list_insert(keys + (size_t)target * k, flags + (size_t)target * k, k, cand);
 }
 
 int orc_iterate(const void* X, int dtype, int64_t n, int d, int metric, int k,
@@ -439,7 +539,8 @@ int orc_iterate(const void* X, int dtype, int64_t n, int d, int metric, int k,
                     st.dist_evals++;
                 }
             }
-        /* Lines 12-18: nearest other NEW sample of each NEW sample u. */
+        /* Lines 12-18: nearest other NEW sample of each NEW sample u.
+         * GNND-r1 (update mode full): every produced pair instead. */
         for (int u = 0; u < m; ++u) {
             uint64_t best = ORC_SENTINEL; /* Alg. 2 line 1: (inf, inf) */
             for (int w = 0; w < m; ++w) {
@@ -447,7 +548,8 @@ int orc_iterate(const void* X, int dtype, int64_t n, int d, int metric, int k,
                 int idx = (u > w) ? u * (u - 1) / 2 + w : w * (w - 1) / 2 + u;
                 if (!Vnn[idx]) continue;
                 uint64_t key = KEY(Dnn[idx], N[w]);
-                if (key < best) best = key;
+                if (g_update_mode == ORC_UPDATE_FULL) offer(keys, flags, k, target_mask, N[u], key, &st);
+                else if (key < best) best = key;
             }
             offer(keys, flags, k, target_mask, N[u], best, &st);
         }
@@ -467,7 +569,8 @@ int orc_iterate(const void* X, int dtype, int64_t n, int d, int metric, int k,
             for (int j = 0; j < q; ++j) {
                 if (!Vno[u * q + j]) continue;
                 uint64_t key = KEY(Dno[u * q + j], O[j]);
-                if (key < best) best = key;
+                if (g_update_mode == ORC_UPDATE_FULL) offer(keys, flags, k, target_mask, N[u], key, &st);
+                else if (key < best) best = key;
             }
             offer(keys, flags, k, target_mask, N[u], best, &st);
         }
@@ -477,7 +580,8 @@ int orc_iterate(const void* X, int dtype, int64_t n, int d, int metric, int k,
             for (int u = 0; u < m; ++u) {
                 if (!Vno[u * q + j]) continue;
                 uint64_t key = KEY(Dno[u * q + j], N[u]);
-                if (key < best) best = key;
+                if (g_update_mode == ORC_UPDATE_FULL) offer(keys, flags, k, target_mask, O[j], key, &st);
+                else if (key < best) best = key;
             }
             offer(keys, flags, k, target_mask, O[j], best, &st);
         }
@@ -517,6 +621,7 @@ int orc_build(const void* X, int dtype, int64_t n, int d, int metric, int k,
               int p, int iters, uint64_t seed, uint32_t* out_ids,
               float* out_dists, orc_stats* per_iter) {
     if (k < 2 || p < 1 || p >= k || iters < 1 || n <= k || d < 1) return ORC_E_USAGE;
+    if (orc_segments(k) < 1) return ORC_E_USAGE;
     uint64_t* keys = (uint64_t*)malloc((size_t)n * k * sizeof(uint64_t));
     uint8_t* flags = (uint8_t*)malloc((size_t)n * k);
     if (!keys || !flags) { free(keys); free(flags); return ORC_E_NOMEM; }
@@ -545,6 +650,7 @@ int orc_ggm_seed(const void* X, int dtype, int64_t n, int d, int metric,
     const int kr = k - kh;       /* replaced/reserved: floor(k/2) */
     const int64_t nB = n - nA;
     if (k < 2 || nA < kr || nB < kr || nA < 1 || nB < 1) return ORC_E_USAGE;
+    if (orc_segments(k) != 1) return ORC_E_USAGE; /* GGM on one-segment lists only */
     dataset ds;
     int rc = ds_open(&ds, X, dtype, n, d, metric);
     if (rc) return rc;

@@ -31,7 +31,8 @@ extern "C" {
 #endif
 
 enum { ORC_OK = 0, ORC_E_USAGE = 1, ORC_E_DOMAIN = 2, ORC_E_NOMEM = 3 };
-enum { ORC_L2SQ = 0, ORC_COSINE = 1 };
+enum { ORC_L2SQ = 0, ORC_COSINE = 1, ORC_CHI2 = 2 };
+enum { ORC_UPDATE_SELECTIVE = 0, ORC_UPDATE_FULL = 1 };
 enum { ORC_F32 = 0, ORC_U8 = 1 };
 
 /* Philox counter tags (D31) */
@@ -56,7 +57,20 @@ void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2],
 /* uniform integer in [0, N): (u64(out1:out0) * N) >> 64  (D31) */
 uint64_t orc_uniform(const uint32_t out[4], uint64_t N);
 
-/* Canonical distance between rows a and b (D4, D5, D6). */
+/* Options (process-wide, test infrastructure):
+ *   "update"        ORC_UPDATE_SELECTIVE (GNND, Alg. 2: the nearest object
+ *                   of each sample) or ORC_UPDATE_FULL (GNND-r1,
+ *                   every produced pair offered to its lists)
+ *   "segment_size"  entries per list segment (32); lists with k >=
+ *                   2 * segment_size are split into k / segment_size
+ *                   segments (D40); smaller k: one segment (D18). */
+int orc_set_option(const char* name, int value);
+int orc_segments(int k);  /* segment count of a k-list; -1 if k is not a multiple */
+/* Segmented InsertIntoNNList: list = sorted union of s
+ * segments, id v in segment v % s.  Returns 1 if inserted, -1 usage. */
+int orc_list_insert_seg(uint64_t* list, uint8_t* flags, int k, int s, uint64_t key);
+
+/* Canonical distance between rows a and b (D4, D5, D6, D39 chi-square). */
 float orc_distance(const void* X, int dtype, int64_t n, int d, int metric,
                    int64_t a, int64_t b);
 

@@ -18,7 +18,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 SENTINEL = np.uint64(0xFFFFFFFFFFFFFFFF)
-L2SQ, COSINE = 0, 1
+L2SQ, COSINE, CHI2 = 0, 1, 2
+UPDATE_SELECTIVE, UPDATE_FULL = 0, 1
 F32, U8 = 0, 1
 
 
@@ -74,6 +75,9 @@ def lib():
         L.orc_phi.restype = dbl
         L.orc_pair_index.argtypes = [i64, P, P]
         L.orc_list_insert.argtypes = [P, P, i32, u64]
+        L.orc_list_insert_seg.argtypes = [P, P, i32, i32, u64]
+        L.orc_set_option.argtypes = [C.c_char_p, i32]
+        L.orc_segments.argtypes = [i32]
         _lib = L
     return _lib
 
@@ -142,6 +146,44 @@ def list_insert(keys: np.ndarray, flags: np.ndarray, key_: int) -> bool:
     """In-place InsertIntoNNList on one list (u64 keys[k], u8 flags[k])."""
     assert keys.dtype == np.uint64 and flags.dtype == np.uint8
     return bool(lib().orc_list_insert(_p(keys), _p(flags), len(keys), int(key_)))
+
+
+def list_insert_seg(keys: np.ndarray, flags: np.ndarray, s: int, key_: int) -> bool:
+    """Segmented InsertIntoNNList on one list kept as the
+    sorted union of s segments (id v in segment v % s)."""
+    assert keys.dtype == np.uint64 and flags.dtype == np.uint8
+    r = lib().orc_list_insert_seg(_p(keys), _p(flags), len(keys), s, int(key_))
+    if r < 0:
+        raise ValueError("bad segment count")
+    return bool(r)
+
+
+def set_option(name: str, value: int):
+    """'update': UPDATE_SELECTIVE (GNND) / UPDATE_FULL (GNND-r1, P:364);
+    'segment_size': entries per list segment (default 32)."""
+    _check(lib().orc_set_option(name.encode(), int(value)), f"set_option {name}")
+
+
+def segments(k: int) -> int:
+    return int(lib().orc_segments(k))
+
+
+class options:
+    """Context manager: temporarily set oracle options, e.g.
+    with orc.options(update=orc.UPDATE_FULL): ..."""
+
+    def __init__(self, **kw):
+        self.kw = kw
+
+    def __enter__(self):
+        for n, v in self.kw.items():
+            set_option(n, v)
+        return self
+
+    def __exit__(self, *a):
+        set_option("update", UPDATE_SELECTIVE)
+        set_option("segment_size", 32)
+        return False
 
 
 # ---------------------------------------------------------------- algorithm
