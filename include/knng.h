@@ -51,7 +51,12 @@ typedef enum {
     KNNG_E_INTERNAL = 6
 } knng_status;
 
-typedef enum { KNNG_L2SQ = 0, KNNG_COSINE = 1 } knng_metric;
+/* KNNG_L2SQ: squared L2 (D4, D5).  KNNG_COSINE: 1 - cos on normalised rows
+ * (D6; float32 only, zero rows -> KNNG_E_DOMAIN).  KNNG_CHI2: chi-square
+ * ("K-Square"), sum (x_i - y_i)^2 / (x_i + y_i) with 0/0 := 0,
+ * evaluated as q = t / s, acc = fmaf(q, t, acc) in dimension order (D39);
+ * components must be >= 0 (else KNNG_E_DOMAIN); CUDA-core tile only. */
+typedef enum { KNNG_L2SQ = 0, KNNG_COSINE = 1, KNNG_CHI2 = 2 } knng_metric;
 typedef enum { KNNG_F32 = 0, KNNG_U8 = 1 } knng_dtype;
 
 /* Per-iteration counters of the device path (host struct). */
@@ -268,6 +273,19 @@ knng_status knng_debug_philox(const uint32_t* ctr, int64_t m, uint64_t seed,
  *                     selection by canonical recomputation inside an
  *                     a-priori error window.
  *                  All produce bit-identical graphs.
+ *   "update"       how the selected neighbours enter the lists (
+ *                  the ablation of P:362-366; all modes are bit-exact
+ *                  against the oracle with the same update definition):
+ *                  0 (default): selective update (Alg. 2), bulk-synchronous
+ *                     lock-free buckets merged once per iteration (D17, D34);
+ *                  1: GNND-r1 -- EVERY produced pair offered to its lists
+ *                     (P:364), immediate insertion under spinlocks
+ *                     (join_locked.cuh); the oracle's update "full";
+ *                  2: GNND as published -- selective, immediate insertion
+ *                     with one spinlock per list segment;
+ *                  3: GNND-r2 -- selective, one spinlock per whole list.
+ *                  Modes 1-3 run one thread block per object.
+ *                  knng_build_sharded always uses 0.
  *   "last_exact_u8" (read-only) 1 if the last build/merge on this thread ran
  *                  on the exact integer path.
  * ---------------------------------------------------------------------- */

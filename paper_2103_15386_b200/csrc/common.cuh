@@ -288,6 +288,16 @@ __device__ __forceinline__ void warp_merge_chunk(Elem& cur, uint64_t cand, Elem*
 }
 
 // ---------------------------------------------------------------- distances
+// metric template values (= knng_metric)
+enum : int { kMetL2 = 0, kMetCos = 1, kMetChi2 = 2 };
+
+__device__ __forceinline__ float chi2_term(float x, float y, float acc) {
+    const float t = x - y;
+    const float s = x + y;
+    const float q = s > 0.0f ? __fdiv_rn(t, s) : 0.0f;
+    return fmaf(q, t, acc);
+}
+
 // Canonical distances (D5/D6): one thread owns one pair and accumulates the
 // dimensions in order 0..d-1: acc = fmaf(x_i - y_i, x_i - y_i, acc).
 template <typename T>
@@ -315,6 +325,13 @@ struct Canon<float> {
                 acc = fmaf(t, t, acc);
             }
         }
+        return acc;
+    }
+    // chi-square ("K-Square"), D39: q = t / s (0 when s = 0),
+    // acc = fmaf(q, t, acc) in dimension order (IEEE division: no fast math)
+    __device__ static __forceinline__ float chi2(const float* __restrict__ a, const float* __restrict__ b, int d) {
+        float acc = 0.0f;
+        for (int i = 0; i < d; ++i) acc = chi2_term(__ldg(a + i), __ldg(b + i), acc);
         return acc;
     }
     // 1 - <x^, y^> on pre-normalised rows, clamped at +0 (D6)

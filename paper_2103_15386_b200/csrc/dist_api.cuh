@@ -144,7 +144,8 @@ knng_status run_sharded(Comm& C, const void* Xloc, int64_t nl, int64_t goff, int
     const size_t rowf = static_cast<size_t>(d) * 4;
     DevBuf Xall(stream);
     const bool try_u8 = metric == KNNG_L2SQ && dt == KNNG_F32 && d <= 258 && g_opt_exact_u8.load();
-    if (!Xall.ensure(static_cast<size_t>(ntot) * (dt == KNNG_U8 && !cosine ? d : rowf)))
+    const bool chi2 = metric == KNNG_CHI2;
+    if (!Xall.ensure(static_cast<size_t>(ntot) * (dt == KNNG_U8 && !cosine && !chi2 ? d : rowf)))
         return fail(KNNG_E_NOMEM, "cannot allocate the vector store");
     char* Xs = Xall.as<char>();
     if (cosine) {
@@ -155,6 +156,11 @@ knng_status run_sharded(Comm& C, const void* Xloc, int64_t nl, int64_t goff, int
         });
         cudaMemcpyAsync(fl + r, fl + P, 4, cudaMemcpyDeviceToDevice, stream);  // 1 -> bit 0 ...
         c.launch("k_flag_shift", [&] { k_flag_shift<<<1, 1, 0, stream>>>(fl + r); });  // ... -> bit 1
+    } else if (chi2 && dt == KNNG_F32) {
+        c.launch("k_check_nonneg", [&] {
+            k_check_nonneg<<<4 * sms, 256, 0, stream>>>(static_cast<const float*>(Xloc), nl * d, fl + r);
+        });
+        c.launch("k_flag_shift", [&] { k_flag_shift<<<1, 1, 0, stream>>>(fl + r); });
     } else if (try_u8) {
         c.launch("k_check_u8", [&] {
             k_check_u8<<<4 * sms, 256, 0, stream>>>(static_cast<const float*>(Xloc), nl * d, fl + r);
@@ -169,14 +175,21 @@ knng_status run_sharded(Comm& C, const void* Xloc, int64_t nl, int64_t goff, int
         all_int &= (f & 1) == 0;
         zero_row |= (f & 2) != 0;
     }
-    if (zero_row) return fail(KNNG_E_DOMAIN, "zero vector under the cosine metric");
+    if (zero_row)
+        return fail(KNNG_E_DOMAIN, cosine ? "zero vector under the cosine metric"
+                                          : "negative value under the chi-square metric");
     if (all_int) dte = KNNG_U8;
+    if (chi2) dte = KNNG_F32;  // chi-square runs on float rows (D39)
     g_last_exact_u8 = all_int;
-    const size_t esz = (dte == KNNG_U8 && !cosine) ? 1 : 4;
+    const size_t esz = (dte == KNNG_U8 && !cosine) ? 1 : 4;  // (chi2: dte is float)
     const size_t rowb = static_cast<size_t>(d) * esz;
     char* Xmine = Xs + static_cast<size_t>(goff) * rowb;
     if (cosine) {
         // normalised rows already in place
+    } else if (chi2 && dt == KNNG_U8) {
+        c.launch("k_u8_to_f32", [&] {
+            k_u8_to_f32<<<4 * sms, 256, 0, stream>>>(static_cast<const uint8_t*>(Xloc), nl * d, reinterpret_cast<float*>(Xmine));
+        });
     } else if (dte == KNNG_U8 && dt == KNNG_F32) {
         c.launch("k_to_u8", [&] {
             k_to_u8<<<4 * sms, 256, 0, stream>>>(static_cast<const float*>(Xloc), nl * d, reinterpret_cast<uint8_t*>(Xmine));
@@ -250,6 +263,9 @@ knng_status run_sharded(Comm& C, const void* Xloc, int64_t nl, int64_t goff, int
         R.xrows = ngrp;
         R.sqn_ext = sqn.p;
         R.bind(ws_buf.as<char>(), nullptr);
+        R.update = 0;  // the distributed refine files through records (bulk update)
+        R.G.lock = nullptr;
+        R.G.imask = nullptr;
         if (cosine) R.Xn = reinterpret_cast<const float*>(R.X);
         R.G.kth = kthall.as<uint64_t>() + base;  // merge_sample writes the own slice ...
         R.G.kth_t = kthall.as<uint64_t>();       // ... the joins read the group's
@@ -271,6 +287,10 @@ knng_status run_sharded(Comm& C, const void* Xloc, int64_t nl, int64_t goff, int
             if (cosine)
                 k_ggm_seed_keys<float, true><<<grid, 256, 256 * 4, stream>>>(nullptr, R.Xn, R.D, nA, ngrp, l, seed,
                                                                           cur.as<uint64_t>(), R.G, reserved);
+            else if (chi2)
+                k_ggm_seed_keys<float, kMetChi2><<<grid, 256, 256 * 4, stream>>>(static_cast<const float*>(R.X), nullptr, R.D,
+                                                                              nA, ngrp, l, seed, cur.as<uint64_t>(), R.G,
+                                                                              reserved);
             else if (dte == KNNG_F32)
                 k_ggm_seed_keys<float, false><<<grid, 256, 256 * 4, stream>>>(static_cast<const float*>(R.X), nullptr, R.D,
                                                                            nA, ngrp, l, seed, cur.as<uint64_t>(), R.G,

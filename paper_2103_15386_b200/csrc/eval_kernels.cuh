@@ -23,11 +23,11 @@ __host__ __device__ inline int bf_stride_elems(int d) {
     return words * 4 / static_cast<int>(sizeof(T));
 }
 
-template <typename T, bool COS>
+template <typename T, int MET>
 __global__ void k_bruteforce(const T* __restrict__ X, const float* __restrict__ Xn, int64_t n, int d,
                              const int64_t* __restrict__ queries, int64_t nq, int kq, uint64_t* out) {
-    using E = typename std::conditional<COS, float, T>::type;
-    const E* __restrict__ V = COS ? reinterpret_cast<const E*>(Xn) : reinterpret_cast<const E*>(X);
+    using E = typename std::conditional<MET == kMetCos, float, T>::type;
+    const E* __restrict__ V = MET == kMetCos ? reinterpret_cast<const E*>(Xn) : reinterpret_cast<const E*>(X);
     extern __shared__ __align__(16) unsigned char bf_smem[];
     const int W = blockDim.x >> 5;
     const int stride = bf_stride_elems<E>(d);
@@ -65,11 +65,15 @@ __global__ void k_bruteforce(const T* __restrict__ X, const float* __restrict__ 
             if (qid[qi] < 0) continue;  // warp-uniform
             const E* qrow = qv + (warp * kBfQPerWarp + qi) * stride;
             float dist;
-            if constexpr (COS) {
+            if constexpr (MET == kMetCos) {
                 float s = 0.0f;
                 for (int j = 0; j < d; ++j) s = fmaf(qrow[j], prow[j], s);
                 const float r = 1.0f - s;
                 dist = r > 0.0f ? r : 0.0f;
+            } else if constexpr (MET == kMetChi2) {
+                float acc = 0.0f;
+                for (int j = 0; j < d; ++j) acc = chi2_term(qrow[j], prow[j], acc);
+                dist = acc;
             } else if constexpr (std::is_same<E, float>::value) {
                 float acc = 0.0f;
                 for (int j = 0; j < d; ++j) {

@@ -13,7 +13,7 @@ namespace knng {
 // One node's seed: `in` = its input entry in lane < k (ascending list);
 // node i (an id of the merge's numbering, local index li of the launch)
 // draws from the other subset [obase, obase + osize).
-template <typename T, bool COS>
+template <typename T, int MET>
 __device__ __forceinline__ void ggm_seed_node(const T* __restrict__ X, const float* __restrict__ Xn, const Dims& D,
                                               int64_t li, int64_t i, uint64_t in, int64_t obase, uint64_t osize,
                                               int level, uint64_t seed, Graph& G, uint64_t* __restrict__ reserved) {
@@ -50,8 +50,10 @@ __device__ __forceinline__ void ggm_seed_node(const T* __restrict__ X, const flo
         e = in << 1;  // kept half: OLD
     } else if (static_cast<int>(lane) < k) {
         float dist;
-        if constexpr (COS) {
+        if constexpr (MET == kMetCos) {
             dist = Canon<float>::cos(Xn + static_cast<size_t>(i) * D.d, Xn + static_cast<size_t>(chosen) * D.d, D.d);
+        } else if constexpr (MET == kMetChi2) {
+            dist = Canon<float>::chi2(X + static_cast<size_t>(i) * D.d, X + static_cast<size_t>(chosen) * D.d, D.d);
         } else {
             dist = Canon<T>::l2(X + static_cast<size_t>(i) * D.d, X + static_cast<size_t>(chosen) * D.d, D.d);
         }
@@ -66,7 +68,7 @@ __device__ __forceinline__ void ggm_seed_node(const T* __restrict__ X, const flo
     if (static_cast<int>(lane) == k - 1) G.kth[li] = ek;
 }
 
-template <typename T, bool COS>
+template <typename T, int MET>
 __global__ void k_ggm_seed(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, int64_t nA, int level,
                            uint64_t seed, const uint32_t* __restrict__ idsA, const float* __restrict__ distsA,
                            const uint32_t* __restrict__ idsB, const float* __restrict__ distsB, Graph G,
@@ -90,13 +92,13 @@ __global__ void k_ggm_seed(const T* __restrict__ X, const float* __restrict__ Xn
             in = make_key(distsB[o], static_cast<uint32_t>(id + nA));
         }
     }
-    ggm_seed_node<T, COS>(X, Xn, D, i, i, in, own_b ? 0 : nA, static_cast<uint64_t>(own_b ? nA : D.n - nA), level,
+    ggm_seed_node<T, MET>(X, Xn, D, i, i, in, own_b ? 0 : nA, static_cast<uint64_t>(own_b ? nA : D.n - nA), level,
                           seed, G, reserved);
 }
 
 // Distributed refine: the launch owns nodes D.base + [0, D.n) of a merge over
 // n_all ids; keys_in holds their lists (merge-numbered ids, ascending).
-template <typename T, bool COS>
+template <typename T, int MET>
 __global__ void k_ggm_seed_keys(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, int64_t nA,
                                 int64_t n_all, int level, uint64_t seed, const uint64_t* __restrict__ keys_in,
                                 Graph G, uint64_t* __restrict__ reserved) {
@@ -105,7 +107,7 @@ __global__ void k_ggm_seed_keys(const T* __restrict__ X, const float* __restrict
     const int64_t i = D.base + li;
     const bool own_b = i >= nA;
     const uint64_t in = static_cast<int>(lane_id()) < D.k ? keys_in[static_cast<size_t>(li) * D.k + lane_id()] : kSentinel;
-    ggm_seed_node<T, COS>(X, Xn, D, li, i, in, own_b ? 0 : nA, static_cast<uint64_t>(own_b ? nA : n_all - nA), level,
+    ggm_seed_node<T, MET>(X, Xn, D, li, i, in, own_b ? 0 : nA, static_cast<uint64_t>(own_b ? nA : n_all - nA), level,
                           seed, G, reserved);
 }
 

@@ -32,6 +32,11 @@ struct Graph {
     uint32_t* rec_tgt;
     uint64_t* rec_key;
     unsigned long long* rec_cnt;
+    // Locked immediate update (join_locked.cuh, the ablation of P:364-366):
+    // per-list (or per-segment) spinlock words and the "entered during this
+    // iteration" bits, one u32 per list segment; nullptr in the bulk path.
+    unsigned int* lock;
+    uint32_t* imask;
 };
 
 struct Samples {
@@ -60,7 +65,7 @@ __device__ __forceinline__ uint32_t kmask_of(int k) { return k >= 32 ? kFull : (
 // Alg. 1 lines 1-4: k distinct random ids != s (D1, D2) drawn in
 // counter order j = 0, 1, ... from Philox(INIT, s, j, s >> 32), canonical
 // distances, sorted by key (D3), all NEW.
-template <typename T, bool COS>
+template <typename T, int MET>
 __global__ void k_init(const T* __restrict__ X, const float* __restrict__ Xn, Dims D,
                        uint64_t seed, Graph G) {
     const int64_t s = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -94,8 +99,10 @@ __global__ void k_init(const T* __restrict__ X, const float* __restrict__ Xn, Di
     uint64_t kk = kSentinel;
     if (static_cast<int>(lane) < k) {
         float dist;
-        if constexpr (COS) {
+        if constexpr (MET == kMetCos) {
             dist = Canon<float>::cos(Xn + static_cast<size_t>(s) * D.d, Xn + static_cast<size_t>(chosen) * D.d, D.d);
+        } else if constexpr (MET == kMetChi2) {
+            dist = Canon<float>::chi2(X + static_cast<size_t>(s) * D.d, X + static_cast<size_t>(chosen) * D.d, D.d);
         } else {
             dist = Canon<T>::l2(X + static_cast<size_t>(s) * D.d, X + static_cast<size_t>(chosen) * D.d, D.d);
         }
@@ -126,6 +133,13 @@ __global__ void __launch_bounds__(256, 8) k_merge_sample(Dims D, Graph G, Sample
     Elem cur{in_list ? G.keys[static_cast<size_t>(s) * k + lane] : kSentinel,
              in_list ? ((mask >> lane) & 1u) : 0u};
     bool changed = false;
+    if (G.imask) {  // locked immediate update: entries that entered last iteration
+        if (lane == 0) {
+            const uint32_t im = G.imask[s];
+            if (im && prev_stats) atomicAdd(&prev_stats->accepted, static_cast<unsigned long long>(__popc(im)));
+            G.imask[s] = 0;
+        }
+    }
     if (do_merge) {
         const uint32_t c = G.bcnt[s];
         if (c > 0) {
@@ -546,6 +560,21 @@ __global__ void k_check_u8(const float* __restrict__ X, int64_t total, int* bad)
         ok &= (v >= 0.0f && v <= 255.0f && v == rintf(v));
     }
     if (__syncthreads_or(!ok) && threadIdx.x == 0) atomicExch(bad, 1);
+}
+
+// chi-square: flag any negative (or NaN) value (D39)
+__global__ void k_check_nonneg(const float* __restrict__ X, int64_t total, int* bad) {
+    bool ok = true;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        ok &= X[i] >= 0.0f;
+    if (__syncthreads_or(!ok) && threadIdx.x == 0) atomicExch(bad, 1);
+}
+
+__global__ void k_u8_to_f32(const uint8_t* __restrict__ X, int64_t total, float* __restrict__ Y) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        Y[i] = static_cast<float>(X[i]);
 }
 
 __global__ void k_to_u8(const float* __restrict__ X, int64_t total, uint8_t* __restrict__ Y) {

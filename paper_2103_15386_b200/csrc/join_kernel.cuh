@@ -63,12 +63,12 @@ __device__ __forceinline__ bool allowed_pair(int64_t boundary, uint32_t a, uint3
 // over the CTA's 64 NB threads, so warps stay full even though a single
 // node's tile has only ~35-100 blocks (the one-node-per-CTA layout left
 // ~40% of the FP lanes idle).
-template <typename T, bool COS, int NB>
+template <typename T, int MET, int NB>
 __global__ void __launch_bounds__(NB * 64, 2)
 k_join(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Samples S, int64_t boundary,
        int aligned16, DevStats* __restrict__ stats) {
     using Cfg = SlabCfg<T>;
-    using E = typename std::conditional<COS, float, T>::type;
+    using E = typename std::conditional<MET == kMetCos, float, T>::type;
     constexpr bool kFloat = std::is_same<E, float>::value;
     using Acc = typename std::conditional<kFloat, float, unsigned int>::type;
     constexpr int SD = Cfg::kDims, RS = Cfg::kStride, CE = Cfg::kChunkElems;
@@ -76,7 +76,7 @@ k_join(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Samples S,
     constexpr int THREADS = NB * 64;
     constexpr int TILE = kMaxSlots * RS;       // elements of one node's stage
     constexpr int ROUNDS = (NB * 100 + THREADS - 1) / THREADS;  // <= 100 blocks per node
-    const E* __restrict__ V = COS ? reinterpret_cast<const E*>(Xn) : reinterpret_cast<const E*>(X);
+    const E* __restrict__ V = MET == kMetCos ? reinterpret_cast<const E*>(Xn) : reinterpret_cast<const E*>(X);
 
     extern __shared__ __align__(16) unsigned char join_smem[];
     E* rows = reinterpret_cast<E*>(join_smem);  // [2][NB][TILE]
@@ -226,11 +226,16 @@ k_join(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Samples S,
                         for (int rr = 0; rr < 4; ++rr)
 #pragma unroll
                             for (int c = 0; c < 4; ++c) {
-                                if constexpr (COS) {
+                                if constexpr (MET == kMetCos) {
                                     acc[r][rr][c] = fmaf(a[rr].x, b[c].x, acc[r][rr][c]);
                                     acc[r][rr][c] = fmaf(a[rr].y, b[c].y, acc[r][rr][c]);
                                     acc[r][rr][c] = fmaf(a[rr].z, b[c].z, acc[r][rr][c]);
                                     acc[r][rr][c] = fmaf(a[rr].w, b[c].w, acc[r][rr][c]);
+                                } else if constexpr (MET == kMetChi2) {
+                                    acc[r][rr][c] = chi2_term(a[rr].x, b[c].x, acc[r][rr][c]);
+                                    acc[r][rr][c] = chi2_term(a[rr].y, b[c].y, acc[r][rr][c]);
+                                    acc[r][rr][c] = chi2_term(a[rr].z, b[c].z, acc[r][rr][c]);
+                                    acc[r][rr][c] = chi2_term(a[rr].w, b[c].w, acc[r][rr][c]);
                                 } else {
                                     float t;
                                     t = a[rr].x - b[c].x; acc[r][rr][c] = fmaf(t, t, acc[r][rr][c]);
@@ -286,7 +291,7 @@ k_join(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Samples S,
                     if (valid) valid = allowed_pair(boundary, nid[u], nid[w]);
                     if (!valid) continue;
                     float dist;
-                    if constexpr (COS) {
+                    if constexpr (MET == kMetCos) {
                         const float x1 = 1.0f - acc[r][rr][c];
                         dist = x1 > 0.0f ? x1 : 0.0f;
                     } else if constexpr (kFloat) {
@@ -346,9 +351,9 @@ k_join(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Samples S,
     }
 }
 
-template <typename T, bool COS, int NB>
+template <typename T, int MET, int NB>
 constexpr size_t join_smem_bytes() {
-    using E = typename std::conditional<COS, float, T>::type;
+    using E = typename std::conditional<MET == kMetCos, float, T>::type;
     return sizeof(E) * 2 * NB * kMaxSlots * SlabCfg<T>::kStride;
 }
 

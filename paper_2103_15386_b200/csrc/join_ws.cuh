@@ -123,9 +123,9 @@ __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* tm, in
 
 
 
-template <typename T, bool COS, int STAGES>
+template <typename T, int MET, int STAGES>
 struct WsCfg {
-    using E = typename std::conditional<COS, float, T>::type;
+    using E = typename std::conditional<MET == kMetCos, float, T>::type;
     static constexpr int SD = SlabCfg<T>::kDims;
     // 128-B row slabs (32 f32 or 128 u8 dims) whose 16-B chunks are
     // XOR-swizzled by (slot >> 2) & 7, so the LDS.128 of lanes on different
@@ -149,16 +149,16 @@ struct WsCfg {
     static_assert(kSmem + 1024 <= 232448, "227 KB dynamic shared memory per CTA (+ 1 KB TMA alignment)");
 };
 
-template <typename T, bool COS, int STAGES>
+template <typename T, int MET, int STAGES>
 __global__ void __launch_bounds__(kWsThreads, 1)
 k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G, Samples S, int64_t boundary,
           unsigned long long* __restrict__ work, DevStats* __restrict__ stats) {
-    using Cfg = WsCfg<T, COS, STAGES>;
+    using Cfg = WsCfg<T, MET, STAGES>;
     using E = typename Cfg::E;
     constexpr bool kFloat = std::is_same<E, float>::value;
     using Acc = typename std::conditional<kFloat, float, unsigned int>::type;
     constexpr int SD = Cfg::SD, RS = Cfg::RS;
-    const E* __restrict__ V = COS ? reinterpret_cast<const E*>(Xn) : reinterpret_cast<const E*>(X);
+    const E* __restrict__ V = MET == kMetCos ? reinterpret_cast<const E*>(Xn) : reinterpret_cast<const E*>(X);
 
     extern __shared__ __align__(128) unsigned char ws_raw[];
     unsigned char* ws_smem = ws_raw;
@@ -616,11 +616,16 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
                         for (int r = 0; r < 4; ++r)
 #pragma unroll
                             for (int c = 0; c < 4; ++c) {
-                                if constexpr (COS) {
+                                if constexpr (MET == kMetCos) {
                                     acc[r][c] = fmaf(a[r].x, bv[c].x, acc[r][c]);
                                     acc[r][c] = fmaf(a[r].y, bv[c].y, acc[r][c]);
                                     acc[r][c] = fmaf(a[r].z, bv[c].z, acc[r][c]);
                                     acc[r][c] = fmaf(a[r].w, bv[c].w, acc[r][c]);
+                                } else if constexpr (MET == kMetChi2) {
+                                    acc[r][c] = chi2_term(a[r].x, bv[c].x, acc[r][c]);
+                                    acc[r][c] = chi2_term(a[r].y, bv[c].y, acc[r][c]);
+                                    acc[r][c] = chi2_term(a[r].z, bv[c].z, acc[r][c]);
+                                    acc[r][c] = chi2_term(a[r].w, bv[c].w, acc[r][c]);
                                 } else {
                                     float tt;
                                     tt = a[r].x - bv[c].x; acc[r][c] = fmaf(tt, tt, acc[r][c]);
@@ -683,7 +688,7 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
                     if (restricted && valid) valid = allowed_pair(boundary, rid[r], cid[c]);
                     if (!valid) continue;
                     float dist;
-                    if constexpr (COS) {
+                    if constexpr (MET == kMetCos) {
                         const float x1 = 1.0f - acc[r][c];
                         dist = x1 > 0.0f ? x1 : 0.0f;
                     } else if constexpr (kFloat) {

@@ -21,6 +21,7 @@
 #include "join_kernel.cuh"
 #include "join_tc.cuh"
 #include "join_tcf.cuh"
+#include "join_locked.cuh"
 #include "join_ws.cuh"
 
 using namespace knng;
@@ -33,6 +34,7 @@ std::atomic<int64_t> g_launches{0};
 std::atomic<int> g_timing{0};
 std::atomic<int> g_opt_exact_u8{1};
 std::atomic<int> g_opt_join_kernel{0};
+std::atomic<int> g_opt_update{0};  // 0 bulk (default), 1 full (GNND-r1), 2 locked, 3 locked, one lock per list
 thread_local int g_last_exact_u8 = 0;
 std::mutex g_time_mu;
 std::map<std::string, std::pair<double, int64_t>> g_times;
@@ -51,7 +53,7 @@ constexpr int kMaxIters = 256;
 
 // ---------------------------------------------------------------- layout
 struct Layout {
-    size_t keys, newmask, kth, bcnt, bucket, fwd, fcnt, rcnt, fpos, off, rsrc, G, gcnt, bsum, cand, stats,
+    size_t keys, newmask, kth, lock, imask, bcnt, bucket, fwd, fcnt, rcnt, fpos, off, rsrc, G, gcnt, bsum, cand, stats,
         xnorm, xu8, sqn, reserved, flag, total;
     bool has_cand;
 };
@@ -60,7 +62,7 @@ int64_t scan_blocks(int64_t n) { return (n + kScanBlock - 1) / kScanBlock; }
 
 size_t align_up(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
-Layout make_layout(int64_t n, int d, int k, int p, bool cosine, bool own_keys, bool merge, bool u8copy = false) {
+Layout make_layout(int64_t n, int d, int k, int p, bool xcopy, bool own_keys, bool merge, bool u8copy = false) {
     Layout L{};
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -70,8 +72,11 @@ Layout make_layout(int64_t n, int d, int k, int p, bool cosine, bool own_keys, b
     };
     const int cap = 2 * p;
     L.keys = own_keys ? take(static_cast<size_t>(n) * k * 8) : 0;
-    L.newmask = take(static_cast<size_t>(n) * 4);
+    L.newmask = take(static_cast<size_t>(n) * (k > 32 ? k / 32 : 1) * 4);
     L.kth = take(static_cast<size_t>(n) * 8);
+    const int segs = k > 32 ? k / 32 : 1;                    // list segments (D40)
+    L.lock = take(static_cast<size_t>(n) * segs * 4);        // locked update (option "update")
+    L.imask = take(static_cast<size_t>(n) * segs * 4);
     L.bcnt = take(static_cast<size_t>(n) * 4);
     // bucket capacity: sum_t [2 (|R_new(t)| + |F_new(t)|) + |R_old(t)| + |F_old(t)|] <= 6 n p
     L.bucket = take(static_cast<size_t>(6) * n * p * 8);
@@ -90,7 +95,7 @@ Layout make_layout(int64_t n, int d, int k, int p, bool cosine, bool own_keys, b
     L.has_cand = g_opt_join_kernel.load() == 1 || d % 16 != 0;
     L.cand = L.has_cand ? take(static_cast<size_t>(n) * 3 * cap * 8) : 0;
     L.stats = take(sizeof(DevStats) * kMaxIters);
-    L.xnorm = cosine ? take(static_cast<size_t>(n) * d * 4) : 0;
+    L.xnorm = xcopy ? take(static_cast<size_t>(n) * d * 4) : 0;  // normalised (cosine) / float (chi2 of u8) rows
     L.reserved = merge ? take(static_cast<size_t>(n) * (k / 2 > 0 ? k / 2 : 1) * 8) : 0;
     L.xu8 = u8copy ? take(static_cast<size_t>(n) * d) : 0;  // exact integer copy (option exact_u8)
     L.sqn = take(static_cast<size_t>(n) * 4);                // exact squared norms (uint8 tensor-core join)
@@ -221,9 +226,16 @@ bool is_device_ptr(const void* p) {
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// rows copied into L.xnorm: normalised rows (cosine, D6), float rows of uint8
+// input (chi-square is evaluated in float, D39)
+bool needs_xcopy(knng_metric metric, knng_dtype dt) {
+    return metric == KNNG_COSINE || (metric == KNNG_CHI2 && dt == KNNG_U8);
+}
+
 knng_status check_common(knng_dtype dt, int64_t n, int32_t d, int32_t k, knng_metric metric, int32_t p) {
     if (dt != KNNG_F32 && dt != KNNG_U8) return fail(KNNG_E_USAGE, "unknown dtype %d", static_cast<int>(dt));
-    if (metric != KNNG_L2SQ && metric != KNNG_COSINE) return fail(KNNG_E_USAGE, "unknown metric %d", static_cast<int>(metric));
+    if (metric != KNNG_L2SQ && metric != KNNG_COSINE && metric != KNNG_CHI2)
+        return fail(KNNG_E_USAGE, "unknown metric %d", static_cast<int>(metric));
     if (metric == KNNG_COSINE && dt != KNNG_F32) return fail(KNNG_E_USAGE, "cosine requires float32 vectors");
     if (d < 1) return fail(KNNG_E_USAGE, "d must be >= 1 (got %d)", d);
     if (k < 2 || k > 32) return fail(KNNG_E_USAGE, "k must be in [2, 32] (got %d)", k);
@@ -250,6 +262,7 @@ struct Run {
     uint64_t seed;
     int64_t boundary = -1;
     bool sqn_ready = false;   // L.sqn holds the exact squared norms of X
+    int update = 0;           // option "update" at bind time
     int64_t xrows = -1;       // rows of X (ids the samples may hold); -1: D.n
     void* sqn_ext = nullptr;  // squared norms of all xrows rows (distributed refine), else L.sqn
     int sms = 148;            // SM count of the current device (persistent grids)
@@ -282,11 +295,15 @@ struct Run {
         S.cand = L.has_cand ? reinterpret_cast<uint64_t*>(ws + L.cand) : nullptr;
         G.boff = S.off + 2 * (D.n + 1);
         G.kth_t = G.kth;
+        update = g_opt_update.load();
+        G.lock = update ? reinterpret_cast<unsigned int*>(ws + L.lock) : nullptr;
+        G.imask = update ? reinterpret_cast<uint32_t*>(ws + L.imask) : nullptr;
         G.rec_tgt = nullptr;
         G.rec_key = nullptr;
         G.rec_cnt = nullptr;
         stats = reinterpret_cast<DevStats*>(ws + L.stats);
         Xn = metric == KNNG_COSINE ? reinterpret_cast<const float*>(ws + L.xnorm) : nullptr;
+        if (metric == KNNG_CHI2) Xn = nullptr;
     }
 
     int warps_grid(int64_t items, int warps_per_block) const {
@@ -303,18 +320,38 @@ struct Run {
         // likewise the joins' planning warps copy whole sample rows (cap ids)
         cudaMemsetAsync(S.G, 0xFF, static_cast<size_t>(2) * D.n * D.cap * 4, c.stream);
         cudaMemsetAsync(stats, 0, sizeof(DevStats) * kMaxIters, c.stream);
+        if (G.lock) {
+            const int segs = D.k > 32 ? D.k / 32 : 1;
+            cudaMemsetAsync(G.lock, 0, static_cast<size_t>(D.n) * segs * 4, c.stream);
+            cudaMemsetAsync(G.imask, 0, static_cast<size_t>(D.n) * segs * 4, c.stream);
+        }
         return true;
     }
 
-    // cosine: normalised copy of the rows (D6); KNNG_E_DOMAIN on a zero row
+    // cosine: normalised copy of the rows (D6); KNNG_E_DOMAIN on a zero row.
+    // chi-square: KNNG_E_DOMAIN on a negative value; uint8 rows are copied
+    // to float (D39)
     knng_status normalize() {
-        if (metric != KNNG_COSINE) return KNNG_OK;
+        if (metric == KNNG_L2SQ) return KNNG_OK;
         int* flag = reinterpret_cast<int*>(ws + L.flag);
         cudaMemsetAsync(flag, 0, 4, c.stream);
-        c.launch("k_normalize", [&] {
-            k_normalize<<<static_cast<int>((D.n + 255) / 256), 256, 0, c.stream>>>(
-                static_cast<const float*>(X), D.n, D.d, const_cast<float*>(Xn), flag);
-        });
+        if (metric == KNNG_COSINE) {
+            c.launch("k_normalize", [&] {
+                k_normalize<<<static_cast<int>((D.n + 255) / 256), 256, 0, c.stream>>>(
+                    static_cast<const float*>(X), D.n, D.d, const_cast<float*>(Xn), flag);
+            });
+        } else if (dt == KNNG_F32) {
+            c.launch("k_check_nonneg", [&] {
+                k_check_nonneg<<<4 * sms, 256, 0, c.stream>>>(static_cast<const float*>(X), D.n * D.d, flag);
+            });
+        } else {
+            float* xf = reinterpret_cast<float*>(ws + L.xnorm);
+            c.launch("k_u8_to_f32", [&] {
+                k_u8_to_f32<<<4 * sms, 256, 0, c.stream>>>(static_cast<const uint8_t*>(X), D.n * D.d, xf);
+            });
+            X = xf;
+            dt = KNNG_F32;
+        }
         int h = 0;
         cudaMemcpyAsync(&h, flag, 4, cudaMemcpyDeviceToHost, c.stream);
         const cudaError_t e = cudaStreamSynchronize(c.stream);
@@ -323,7 +360,8 @@ struct Run {
             c.err_where = "normalize";
         }
         if (c.err != cudaSuccess) return KNNG_OK;  // reported by finish()
-        if (h) return fail(KNNG_E_DOMAIN, "zero vector under the cosine metric");
+        if (h && metric == KNNG_COSINE) return fail(KNNG_E_DOMAIN, "zero vector under the cosine metric");
+        if (h) return fail(KNNG_E_DOMAIN, "negative value under the chi-square metric");
         return KNNG_OK;
     }
 
@@ -361,6 +399,8 @@ struct Run {
         c.launch("k_init", [&] {
             if (metric == KNNG_COSINE)
                 k_init<float, true><<<grid, wpb * 32, wpb * 32 * 4, c.stream>>>(nullptr, Xn, D, seed, G);
+            else if (metric == KNNG_CHI2)
+                k_init<float, kMetChi2><<<grid, wpb * 32, wpb * 32 * 4, c.stream>>>(static_cast<const float*>(X), nullptr, D, seed, G);
             else if (dt == KNNG_F32)
                 k_init<float, false><<<grid, wpb * 32, wpb * 32 * 4, c.stream>>>(static_cast<const float*>(X), nullptr, D, seed, G);
             else
@@ -408,6 +448,31 @@ struct Run {
         constexpr int NB = kJoinNodes;
         const int jk = g_opt_join_kernel.load();
         const bool force_v3 = jk == 1;
+        if (update) {
+            // the paper's immediate update under spinlocks (join_locked.cuh):
+            // GNND-r1 (full), GNND (segment locks), GNND-r2 (one lock)
+            const int one = update == 3;
+            const int g2 = static_cast<int>(D.n < 16ll * sms * 32 ? D.n : 16ll * sms * 32);
+            c.launch("k_join", [&] {
+                if (metric == KNNG_COSINE) {
+                    if (update == 1) k_join_locked<float, kMetCos, true><<<g2, kLkThreads, 0, c.stream>>>(nullptr, Xn, D, G, S, boundary, one, st);
+                    else k_join_locked<float, kMetCos, false><<<g2, kLkThreads, 0, c.stream>>>(nullptr, Xn, D, G, S, boundary, one, st);
+                } else if (metric == KNNG_CHI2) {
+                    const float* Xf = static_cast<const float*>(X);
+                    if (update == 1) k_join_locked<float, kMetChi2, true><<<g2, kLkThreads, 0, c.stream>>>(Xf, nullptr, D, G, S, boundary, one, st);
+                    else k_join_locked<float, kMetChi2, false><<<g2, kLkThreads, 0, c.stream>>>(Xf, nullptr, D, G, S, boundary, one, st);
+                } else if (dt == KNNG_F32) {
+                    const float* Xf = static_cast<const float*>(X);
+                    if (update == 1) k_join_locked<float, kMetL2, true><<<g2, kLkThreads, 0, c.stream>>>(Xf, nullptr, D, G, S, boundary, one, st);
+                    else k_join_locked<float, kMetL2, false><<<g2, kLkThreads, 0, c.stream>>>(Xf, nullptr, D, G, S, boundary, one, st);
+                } else {
+                    const uint8_t* Xu = static_cast<const uint8_t*>(X);
+                    if (update == 1) k_join_locked<uint8_t, kMetL2, true><<<g2, kLkThreads, 0, c.stream>>>(Xu, nullptr, D, G, S, boundary, one, st);
+                    else k_join_locked<uint8_t, kMetL2, false><<<g2, kLkThreads, 0, c.stream>>>(Xu, nullptr, D, G, S, boundary, one, st);
+                }
+            });
+            return true;
+        }
         const bool u8_slab = al && metric == KNNG_L2SQ && dt == KNNG_U8 && D.d <= kTcRowBytes && D.d % 16 == 0;
         if (u8_slab && jk == 0) {
             // uint8 rows of one 128-B slab: Gram tiles on the tensor cores
@@ -439,7 +504,7 @@ struct Run {
             });
             return true;
         }
-        const bool f32_tc = al && (metric == KNNG_COSINE || dt == KNNG_F32) && D.d % 4 == 0 && D.d <= 128;
+        const bool f32_tc = al && metric != KNNG_CHI2 && (metric == KNNG_COSINE || dt == KNNG_F32) && D.d % 4 == 0 && D.d <= 128;
         if (f32_tc && jk == 4) {
             // float rows: TF32 Gram tiles on the tensor cores, exact selection
             // by canonical recomputation inside the error-bound window.  Opt-in:
@@ -486,6 +551,11 @@ struct Run {
                     constexpr size_t sm = WsCfg<float, true, STG>::kSmem;
                     cudaFuncSetAttribute(k_join_ws<float, true, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
                     k_join_ws<float, true, STG><<<sms, kWsThreads, sm, c.stream>>>(nullptr, Xn, D, G, S, boundary, work, st);
+                } else if (metric == KNNG_CHI2) {
+                    constexpr size_t sm = WsCfg<float, kMetChi2, STG>::kSmem;
+                    cudaFuncSetAttribute(k_join_ws<float, kMetChi2, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+                    k_join_ws<float, kMetChi2, STG><<<sms, kWsThreads, sm, c.stream>>>(static_cast<const float*>(X), nullptr,
+                                                                                       D, G, S, boundary, work, st);
                 } else if (dt == KNNG_F32) {
                     constexpr size_t sm = WsCfg<float, false, STG>::kSmem;
                     cudaFuncSetAttribute(k_join_ws<float, false, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
@@ -516,6 +586,11 @@ struct Run {
                 constexpr size_t sm = join_smem_bytes<float, true, NB>();
                 cudaFuncSetAttribute(k_join<float, true, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
                 k_join<float, true, NB><<<grid, NB * 64, sm, c.stream>>>(nullptr, Xn, D, S, boundary, al, st);
+            } else if (metric == KNNG_CHI2) {
+                constexpr size_t sm = join_smem_bytes<float, kMetChi2, NB>();
+                cudaFuncSetAttribute(k_join<float, kMetChi2, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+                k_join<float, kMetChi2, NB><<<grid, NB * 64, sm, c.stream>>>(static_cast<const float*>(X), nullptr, D, S,
+                                                                            boundary, al, st);
             } else if (dt == KNNG_F32) {
                 constexpr size_t sm = join_smem_bytes<float, false, NB>();
                 cudaFuncSetAttribute(k_join<float, false, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
@@ -619,7 +694,7 @@ extern "C" {
 size_t knng_build_workspace_bytes(knng_dtype dt, int64_t n, int32_t d, int32_t k, int32_t sample_size,
                                   knng_metric metric) {
     if (check_common(dt, n, d, k, metric, sample_size) != KNNG_OK) return 0;
-    return make_layout(n, d, k, sample_size, metric == KNNG_COSINE, true, false, dt == KNNG_F32 && metric == KNNG_L2SQ).total;
+    return make_layout(n, d, k, sample_size, needs_xcopy(metric, dt), true, false, dt == KNNG_F32 && metric == KNNG_L2SQ).total;
 }
 
 knng_status knng_build(const void* vectors, knng_dtype dt, int64_t n, int32_t d, int32_t k, knng_metric metric,
@@ -635,7 +710,7 @@ knng_status knng_build(const void* vectors, knng_dtype dt, int64_t n, int32_t d,
     c.stream = static_cast<cudaStream_t>(stream);
     c.timing = g_timing.load() != 0;
     Run R(c);
-    R.L = make_layout(n, d, k, sample_size, metric == KNNG_COSINE, true, false, dt == KNNG_F32 && metric == KNNG_L2SQ);
+    R.L = make_layout(n, d, k, sample_size, needs_xcopy(metric, dt), true, false, dt == KNNG_F32 && metric == KNNG_L2SQ);
     char* ws = nullptr;
     if ((s = get_workspace(c, workspace, workspace_bytes, R.L.total, &ws))) return s;
     R.D = Dims{n, d, k, sample_size, 2 * sample_size};
@@ -696,7 +771,7 @@ knng_status knng_bruteforce(const void* vectors, knng_dtype dt, int64_t n, int32
                             const int64_t* queries, int64_t nq, int32_t kq, uint32_t* out_ids, float* out_dists,
                             void* stream) {
     if (dt != KNNG_F32 && dt != KNNG_U8) return fail(KNNG_E_USAGE, "unknown dtype");
-    if (metric != KNNG_L2SQ && metric != KNNG_COSINE) return fail(KNNG_E_USAGE, "unknown metric");
+    if (metric != KNNG_L2SQ && metric != KNNG_COSINE && metric != KNNG_CHI2) return fail(KNNG_E_USAGE, "unknown metric");
     if (metric == KNNG_COSINE && dt != KNNG_F32) return fail(KNNG_E_USAGE, "cosine requires float32 vectors");
     if (kq < 1 || kq > 32 || n <= kq || d < 1 || nq < 0) return fail(KNNG_E_USAGE, "bad bruteforce arguments");
     if (nq == 0) return KNNG_OK;
@@ -705,16 +780,32 @@ knng_status knng_bruteforce(const void* vectors, knng_dtype dt, int64_t n, int32
     Ctx c;
     c.stream = static_cast<cudaStream_t>(stream);
     c.timing = g_timing.load() != 0;
-    const bool cosine = metric == KNNG_COSINE;
-    const size_t esz = (cosine || dt == KNNG_F32) ? 4 : 1;
+    const bool cosine = metric == KNNG_COSINE, chi2 = metric == KNNG_CHI2;
+    const size_t esz = (cosine || chi2 || dt == KNNG_F32) ? 4 : 1;
     const size_t outb = static_cast<size_t>(nq) * kq * 8;
-    const size_t xnb = cosine ? static_cast<size_t>(n) * d * 4 : 0;
+    const size_t xnb = needs_xcopy(metric, dt) ? static_cast<size_t>(n) * d * 4 : 0;
     char* ws = nullptr;
     knng_status s;
     if ((s = get_workspace(c, nullptr, 0, align_up(outb) + align_up(xnb) + 256, &ws))) return s;
     uint64_t* keys = reinterpret_cast<uint64_t*>(ws);
-    float* Xn = cosine ? reinterpret_cast<float*>(ws + align_up(outb)) : nullptr;
+    float* Xn = xnb ? reinterpret_cast<float*>(ws + align_up(outb)) : nullptr;
     int* flag = reinterpret_cast<int*>(ws + align_up(outb) + align_up(xnb));
+    const float* Xf = static_cast<const float*>(vectors);  // chi-square rows (float)
+    if (chi2) {
+        cudaMemsetAsync(flag, 0, 4, c.stream);
+        if (dt == KNNG_U8) {
+            c.launch("k_u8_to_f32", [&] {
+                k_u8_to_f32<<<592, 256, 0, c.stream>>>(static_cast<const uint8_t*>(vectors), n * d, Xn);
+            });
+            Xf = Xn;
+        } else {
+            c.launch("k_check_nonneg", [&] { k_check_nonneg<<<592, 256, 0, c.stream>>>(Xf, n * d, flag); });
+            int h = 0;
+            cudaMemcpyAsync(&h, flag, 4, cudaMemcpyDeviceToHost, c.stream);
+            cudaStreamSynchronize(c.stream);
+            if (h) return fail(KNNG_E_DOMAIN, "negative value under the chi-square metric");
+        }
+    }
     if (cosine) {
         cudaMemsetAsync(flag, 0, 4, c.stream);
         c.launch("k_normalize", [&] {
@@ -740,6 +831,9 @@ knng_status knng_bruteforce(const void* vectors, knng_dtype dt, int64_t n, int32
         if (cosine) {
             cudaFuncSetAttribute(k_bruteforce<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
             k_bruteforce<float, true><<<grid, W * 32, smem, c.stream>>>(nullptr, Xn, n, d, queries, nq, kq, keys);
+        } else if (chi2) {
+            cudaFuncSetAttribute(k_bruteforce<float, kMetChi2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            k_bruteforce<float, kMetChi2><<<grid, W * 32, smem, c.stream>>>(Xf, nullptr, n, d, queries, nq, kq, keys);
         } else if (dt == KNNG_F32) {
             cudaFuncSetAttribute(k_bruteforce<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
             k_bruteforce<float, false><<<grid, W * 32, smem, c.stream>>>(static_cast<const float*>(vectors), nullptr, n, d,
@@ -768,7 +862,7 @@ knng_status knng_debug_init(const void* vectors, knng_dtype dt, int64_t n, int32
     c.stream = static_cast<cudaStream_t>(stream);
     c.timing = g_timing.load() != 0;
     Run R(c);
-    R.L = make_layout(n, d, k, 1, metric == KNNG_COSINE, false, false, dt == KNNG_F32 && metric == KNNG_L2SQ);
+    R.L = make_layout(n, d, k, 1, needs_xcopy(metric, dt), false, false, dt == KNNG_F32 && metric == KNNG_L2SQ);
     char* ws = nullptr;
     if ((s = get_workspace(c, nullptr, 0, R.L.total, &ws))) return s;
     R.D = Dims{n, d, k, 1, 2};
@@ -798,7 +892,7 @@ knng_status knng_debug_iterate(const void* vectors, knng_dtype dt, int64_t n, in
     c.stream = static_cast<cudaStream_t>(stream);
     c.timing = g_timing.load() != 0;
     Run R(c);
-    R.L = make_layout(n, d, k, sample_size, metric == KNNG_COSINE, false, false, dt == KNNG_F32 && metric == KNNG_L2SQ);
+    R.L = make_layout(n, d, k, sample_size, needs_xcopy(metric, dt), false, false, dt == KNNG_F32 && metric == KNNG_L2SQ);
     char* ws = nullptr;
     if ((s = get_workspace(c, workspace, workspace_bytes, R.L.total, &ws))) return s;
     R.D = Dims{n, d, k, sample_size, 2 * sample_size};
@@ -873,7 +967,7 @@ size_t knng_merge_workspace_bytes(knng_dtype dt, int64_t nA, int64_t nB, int32_t
     if (check_common(dt, nA + nB, d, k, metric, sample_size) != KNNG_OK) return 0;
     const int64_t n = nA + nB;
     const size_t vbytes = static_cast<size_t>(n) * d * (dt == KNNG_F32 ? 4 : 1);
-    return make_layout(n, d, k, sample_size, metric == KNNG_COSINE, true, true, dt == KNNG_F32 && metric == KNNG_L2SQ).total + align_up(vbytes);
+    return make_layout(n, d, k, sample_size, needs_xcopy(metric, dt), true, true, dt == KNNG_F32 && metric == KNNG_L2SQ).total + align_up(vbytes);
 }
 
 knng_status knng_merge(const void* vecA, int64_t nA, const uint32_t* idsA, const float* distsA, const void* vecB,
@@ -897,7 +991,7 @@ knng_status knng_merge(const void* vecA, int64_t nA, const uint32_t* idsA, const
     c.stream = static_cast<cudaStream_t>(stream);
     c.timing = g_timing.load() != 0;
     Run R(c);
-    R.L = make_layout(n, d, k, sample_size, metric == KNNG_COSINE, true, true, dt == KNNG_F32 && metric == KNNG_L2SQ);
+    R.L = make_layout(n, d, k, sample_size, needs_xcopy(metric, dt), true, true, dt == KNNG_F32 && metric == KNNG_L2SQ);
     const size_t esz = dt == KNNG_F32 ? 4 : 1;
     const size_t vbytes = static_cast<size_t>(n) * d * esz;
     char* ws = nullptr;
@@ -930,6 +1024,9 @@ knng_status knng_merge(const void* vecA, int64_t nA, const uint32_t* idsA, const
         if (metric == KNNG_COSINE)
             k_ggm_seed<float, true><<<grid, 256, 256 * 4, c.stream>>>(nullptr, R.Xn, R.D, nA, level, seed, idsA, distsA, idsB,
                                                                 distsB, R.G, reserved, bad);
+        else if (metric == KNNG_CHI2)
+            k_ggm_seed<float, kMetChi2><<<grid, 256, 256 * 4, c.stream>>>(reinterpret_cast<const float*>(R.X), nullptr, R.D, nA,
+                                                                     level, seed, idsA, distsA, idsB, distsB, R.G, reserved, bad);
         else if (R.dt == KNNG_F32)
             k_ggm_seed<float, false><<<grid, 256, 256 * 4, c.stream>>>(reinterpret_cast<const float*>(R.X), nullptr, R.D, nA,
                                                                  level, seed, idsA, distsA, idsB, distsB, R.G, reserved, bad);
@@ -1125,6 +1222,11 @@ knng_status knng_set_option(const char* name, int64_t value) {
         g_opt_exact_u8.store(value ? 1 : 0);
         return KNNG_OK;
     }
+    if (strcmp(name, "update") == 0) {
+        if (value < 0 || value > 3) return fail(KNNG_E_USAGE, "update must be in [0, 3]");
+        g_opt_update.store(static_cast<int>(value));
+        return KNNG_OK;
+    }
     if (strcmp(name, "join_kernel") == 0) {
         if (value < 0 || value > 4 || value == 3) return fail(KNNG_E_USAGE, "join_kernel must be 0, 1, 2 or 4");
         g_opt_join_kernel.store(static_cast<int>(value));
@@ -1137,6 +1239,7 @@ knng_status knng_get_option(const char* name, int64_t* host_value) {
     if (!name || !host_value) return fail(KNNG_E_USAGE, "null argument");
     if (strcmp(name, "exact_u8") == 0) *host_value = g_opt_exact_u8.load();
     else if (strcmp(name, "join_kernel") == 0) *host_value = g_opt_join_kernel.load();
+    else if (strcmp(name, "update") == 0) *host_value = g_opt_update.load();
     else if (strcmp(name, "last_exact_u8") == 0) *host_value = g_last_exact_u8;
     else return fail(KNNG_E_USAGE, "unknown option '%s'", name);
     return KNNG_OK;

@@ -17,9 +17,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libknng.so")
 
 KNNG_OK, KNNG_E_USAGE, KNNG_E_DOMAIN, KNNG_E_NOMEM, KNNG_E_CUDA, KNNG_E_NCCL, KNNG_E_INTERNAL = range(7)
-KNNG_L2SQ, KNNG_COSINE = 0, 1
+KNNG_L2SQ, KNNG_COSINE, KNNG_CHI2 = 0, 1, 2
 KNNG_F32, KNNG_U8 = 0, 1
-METRICS = {"l2": KNNG_L2SQ, "l2sq": KNNG_L2SQ, "cosine": KNNG_COSINE}
+METRICS = {"l2": KNNG_L2SQ, "l2sq": KNNG_L2SQ, "cosine": KNNG_COSINE, "chi2": KNNG_CHI2}
 
 
 class KnngError(RuntimeError):
