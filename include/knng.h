@@ -27,8 +27,11 @@
  *    distance equals a recomputed one bit for bit; u8 distances are exact
  *    integers stored as float.
  *  - Determinism: outputs are a pure function of (inputs, parameters, seed).
- *  - Limits of this version: 2 <= k <= 32, 1 <= sample_size(p) < k,
- *    2p <= 32 (p <= 16), n < 2^32 - 1, n > k, n * p < 2^32.
+ *  - Limits of this version: 2 <= k <= 32, or k = 64, 96, 128 as segmented
+ *    lists (D40: k / 32 segments of 32 entries, id v in segment
+ *    v % (k/32); knng_build and the debug ABI only -- the GGM merge takes
+ *    one-segment lists); 1 <= sample_size(p) < k, 2p <= 32 (p <= 16),
+ *    n < 2^32 - 1, n > k (segmented: n >= k + k/32), n * p < 2^32.
  */
 #ifndef KNNG_H
 #define KNNG_H

@@ -22,6 +22,7 @@
 #include "join_tc.cuh"
 #include "join_tcf.cuh"
 #include "join_locked.cuh"
+#include "seg_kernels.cuh"
 #include "join_ws.cuh"
 
 using namespace knng;
@@ -238,10 +239,13 @@ knng_status check_common(knng_dtype dt, int64_t n, int32_t d, int32_t k, knng_me
         return fail(KNNG_E_USAGE, "unknown metric %d", static_cast<int>(metric));
     if (metric == KNNG_COSINE && dt != KNNG_F32) return fail(KNNG_E_USAGE, "cosine requires float32 vectors");
     if (d < 1) return fail(KNNG_E_USAGE, "d must be >= 1 (got %d)", d);
-    if (k < 2 || k > 32) return fail(KNNG_E_USAGE, "k must be in [2, 32] (got %d)", k);
+    if (k < 2 || (k > 32 && (k % 32 != 0 || k > 128)))
+        return fail(KNNG_E_USAGE, "k must be in [2, 32] or 64, 96, 128 (segmented lists, P:246) (got %d)", k);
     if (p < 1 || p >= k) return fail(KNNG_E_USAGE, "sample_size must satisfy 1 <= p < k (got p=%d, k=%d)", p, k);
     if (2 * p > 32) return fail(KNNG_E_USAGE, "sample_size must be <= 16 in this version (got %d)", p);
     if (n <= k) return fail(KNNG_E_USAGE, "n must exceed k (n=%lld, k=%d)", static_cast<long long>(n), k);
+    if (k > 32 && n < k + k / 32)
+        return fail(KNNG_E_USAGE, "segmented lists need n >= k + k/32 (each residue class holds 32 others)");
     if (n >= 0xFFFFFFFFll) return fail(KNNG_E_USAGE, "n must be < 2^32 - 1");
     if (n * static_cast<int64_t>(p) >= (1ll << 32)) return fail(KNNG_E_USAGE, "n * sample_size must be < 2^32");
     return KNNG_OK;
@@ -393,9 +397,32 @@ struct Run {
         g_last_exact_u8 = 1;
     }
 
+    int segs() const { return D.k > 32 ? D.k / 32 : 1; }
+
+    template <int SEG>
+    void init_seg(int grid, int wpb) {
+        const size_t sm = static_cast<size_t>(wpb) * 32 * 4;
+        if (metric == KNNG_COSINE)
+            k_init_seg<float, kMetCos, SEG><<<grid, wpb * 32, sm, c.stream>>>(nullptr, Xn, D, seed, G);
+        else if (metric == KNNG_CHI2)
+            k_init_seg<float, kMetChi2, SEG><<<grid, wpb * 32, sm, c.stream>>>(static_cast<const float*>(X), nullptr, D, seed, G);
+        else if (dt == KNNG_F32)
+            k_init_seg<float, kMetL2, SEG><<<grid, wpb * 32, sm, c.stream>>>(static_cast<const float*>(X), nullptr, D, seed, G);
+        else
+            k_init_seg<uint8_t, kMetL2, SEG><<<grid, wpb * 32, sm, c.stream>>>(static_cast<const uint8_t*>(X), nullptr, D, seed, G);
+    }
+
     void init() {
         const int wpb = 8;
         const int grid = warps_grid(D.n, wpb);
+        if (segs() > 1) {  // segmented lists (D40)
+            c.launch("k_init", [&] {
+                if (segs() == 2) init_seg<2>(grid, wpb);
+                else if (segs() == 3) init_seg<3>(grid, wpb);
+                else init_seg<4>(grid, wpb);
+            });
+            return;
+        }
         c.launch("k_init", [&] {
             if (metric == KNNG_COSINE)
                 k_init<float, true><<<grid, wpb * 32, wpb * 32 * 4, c.stream>>>(nullptr, Xn, D, seed, G);
@@ -413,8 +440,57 @@ struct Run {
         const int wpb = 8;
         const int grid = warps_grid(D.n, wpb);
         DevStats* ps = prev_iter >= 0 ? stats + prev_iter : nullptr;
+        const int sg = segs();
         c.launch(do_sample ? "k_merge_sample" : "k_merge", [&] {
-            k_merge_sample<<<grid, wpb * 32, wpb * 64 * sizeof(uint64_t), c.stream>>>(D, G, S, do_merge, do_sample, ps);
+            const size_t sm = static_cast<size_t>(wpb) * (sg * 32 + 32) * sizeof(uint64_t);
+            if (sg == 2) k_merge_sample_seg<2><<<grid, wpb * 32, sm, c.stream>>>(D, G, S, do_merge, do_sample, ps);
+            else if (sg == 3) k_merge_sample_seg<3><<<grid, wpb * 32, sm, c.stream>>>(D, G, S, do_merge, do_sample, ps);
+            else if (sg == 4) k_merge_sample_seg<4><<<grid, wpb * 32, sm, c.stream>>>(D, G, S, do_merge, do_sample, ps);
+            else k_merge_sample<<<grid, wpb * 32, wpb * 64 * sizeof(uint64_t), c.stream>>>(D, G, S, do_merge, do_sample, ps);
+        });
+    }
+
+    // segment-major state -> merged list: ids/dists and/or keys/flags
+    void export_seg(uint32_t* ids, float* dists, uint64_t* keys_out, uint8_t* flags_out) {
+        const int sg = segs(), wpb = 8, grid = warps_grid(D.n, wpb);
+        const size_t sm = static_cast<size_t>(wpb) * sg * 32 * 8;
+        c.launch("k_export", [&] {
+            if (sg == 2) k_export_seg<2><<<grid, wpb * 32, sm, c.stream>>>(D, G, ids, dists, keys_out, flags_out);
+            else if (sg == 3) k_export_seg<3><<<grid, wpb * 32, sm, c.stream>>>(D, G, ids, dists, keys_out, flags_out);
+            else k_export_seg<4><<<grid, wpb * 32, sm, c.stream>>>(D, G, ids, dists, keys_out, flags_out);
+        });
+    }
+    void state_in(const uint64_t* keys_in, const uint8_t* flags) {
+        const int sg = segs(), wpb = 8, grid = warps_grid(D.n, wpb);
+        if (sg == 1) {
+            c.launch("k_state_in", [&] { k_state_in<<<grid, 256, 0, c.stream>>>(D, G, flags); });
+            return;
+        }
+        const size_t sm = static_cast<size_t>(wpb) * sg * (32 * 8 + 4);
+        c.launch("k_state_in", [&] {
+            if (sg == 2) k_state_in_seg<2><<<grid, wpb * 32, sm, c.stream>>>(D, G, keys_in, flags);
+            else if (sg == 3) k_state_in_seg<3><<<grid, wpb * 32, sm, c.stream>>>(D, G, keys_in, flags);
+            else k_state_in_seg<4><<<grid, wpb * 32, sm, c.stream>>>(D, G, keys_in, flags);
+        });
+    }
+    void state_out(uint64_t* keys_out, uint8_t* flags) {
+        if (segs() > 1) {
+            // the merged list is written to a scratch copy first: keys_out may
+            // be the buffer the segment-major state lives in
+            void* tmp = nullptr;
+            if (cudaMallocAsync(&tmp, static_cast<size_t>(D.n) * D.k * 8, c.stream) != cudaSuccess) {
+                cudaGetLastError();
+                c.err = cudaErrorMemoryAllocation;
+                c.err_where = "state export";
+                return;
+            }
+            export_seg(nullptr, nullptr, static_cast<uint64_t*>(tmp), flags);
+            cudaMemcpyAsync(keys_out, tmp, static_cast<size_t>(D.n) * D.k * 8, cudaMemcpyDeviceToDevice, c.stream);
+            cudaFreeAsync(tmp, c.stream);
+            return;
+        }
+        c.launch("k_state_out", [&] {
+            k_state_out<<<static_cast<int>((D.n * D.k + 255) / 256), 256, 0, c.stream>>>(D, G, flags);
         });
     }
 
@@ -621,6 +697,10 @@ struct Run {
     }
 
     void export_graph(uint32_t* ids, float* dists) {
+        if (segs() > 1) {
+            export_seg(ids, dists, nullptr, nullptr);
+            return;
+        }
         const int64_t total = D.n * D.k;
         c.launch("k_export", [&] {
             k_export<<<static_cast<int>((total + 255) / 256), 256, 0, c.stream>>>(G.keys, total, ids, dists);
@@ -874,9 +954,7 @@ knng_status knng_debug_init(const void* vectors, knng_dtype dt, int64_t n, int32
     if ((s = R.normalize())) return s;
     R.compress();
     R.init();
-    c.launch("k_state_out", [&] {
-        k_state_out<<<static_cast<int>((n * k + 255) / 256), 256, 0, c.stream>>>(R.D, R.G, flags);
-    });
+    R.state_out(keys, flags);
     return c.finish();
 }
 
@@ -905,14 +983,10 @@ knng_status knng_debug_iterate(const void* vectors, knng_dtype dt, int64_t n, in
     R.zero_state();
     if ((s = R.normalize())) return s;
     R.compress();
-    c.launch("k_state_in", [&] {
-        k_state_in<<<R.warps_grid(n, 8), 256, 0, c.stream>>>(R.D, R.G, flags);
-    });
+    R.state_in(keys, flags);
     R.iteration(0, tword, false);
     R.merge_sample(1, 0, 0);
-    c.launch("k_state_out", [&] {
-        k_state_out<<<static_cast<int>((n * k + 255) / 256), 256, 0, c.stream>>>(R.D, R.G, flags);
-    });
+    R.state_out(keys, flags);
     R.collect_stats(1);
     if (host_stats && !g_last_stats.empty()) *host_stats = g_last_stats[0];
     return c.finish();
@@ -938,9 +1012,7 @@ knng_status knng_debug_sample(int64_t n, int32_t k, int32_t sample_size, uint32_
     R.bind(ws, nullptr);
     R.zero_state();
     cudaMemcpyAsync(R.G.keys, keys, static_cast<size_t>(n) * k * 8, cudaMemcpyDeviceToDevice, c.stream);
-    c.launch("k_state_in", [&] {
-        k_state_in<<<R.warps_grid(n, 8), 256, 0, c.stream>>>(R.D, R.G, flags);
-    });
+    R.state_in(R.G.keys, flags);
     R.merge_sample(0, 1, -1);
     R.reverse(tword);
     c.launch("k_samples_out", [&] {
@@ -977,6 +1049,7 @@ knng_status knng_merge(const void* vecA, int64_t nA, const uint32_t* idsA, const
     const int64_t n = nA + nB;
     knng_status s = check_common(dt, n, d, k, metric, sample_size);
     if (s) return s;
+    if (k > 32) return fail(KNNG_E_USAGE, "GGM merges one-segment lists (k <= 32)");
     const int kr = k / 2;
     if (nA < kr || nB < kr || nA < 1 || nB < 1)
         return fail(KNNG_E_USAGE, "each graph needs at least floor(k/2) = %d nodes (nA=%lld, nB=%lld)", kr,
@@ -1064,6 +1137,7 @@ knng_status knng_extend(const void* vec_old, int64_t n_old, const uint32_t* ids_
     knng_status s = check_common(dt, n_new, d, k, metric, sample_size);
     if (s) return s;
     if ((s = check_common(dt, n_old + n_new, d, k, metric, sample_size))) return s;
+    if (k > 32) return fail(KNNG_E_USAGE, "GGM merges one-segment lists (k <= 32)");
     if (n_old <= k) return fail(KNNG_E_USAGE, "the existing graph needs n_old > k");
     if (iters < 1 || iters > kMaxIters) return fail(KNNG_E_USAGE, "iters must be in [1, %d]", kMaxIters);
     if (!is_device_ptr(vec_new) || !is_device_ptr(out_ids) || !is_device_ptr(out_dists))
@@ -1153,6 +1227,7 @@ knng_status knng_build_sharded(void* comm, const void* local_vectors, int64_t n_
     Comm& C = *static_cast<Comm*>(comm);
     knng_status s = check_common(dt, n_local, d, k, metric, sample_size);
     if (s) return s;
+    if (k > 32 && C.world > 1) return fail(KNNG_E_USAGE, "the GGM tree merges one-segment lists (k <= 32)");
     if (C.world & (C.world - 1)) return fail(KNNG_E_USAGE, "the world size must be a power of two");
     if (n_total != n_local * C.world) return fail(KNNG_E_USAGE, "n_total must be world * n_local (equal shards)");
     if (global_offset != static_cast<int64_t>(C.rank) * n_local)
