@@ -55,6 +55,11 @@ def parse():
                     help="GGM refine iterations: one count, or one per tree level (N>1); the N=1 GGM "
                          "line uses the first")
     ap.add_argument("--no-ggm", action="store_true", help="skip the N=1 GGM measurement")
+    ap.add_argument("--deep-rows", type=int, default=50_000_000,
+                    help="N=1 DEEP-shaped (continuous fp32, d=96) line: rows (0 = skip)")
+    ap.add_argument("--deep-iters", type=int, default=8)
+    ap.add_argument("--deep-steps", type=int, default=2)
+    ap.add_argument("--deep-warmup", type=int, default=1)
     return ap.parse_args()
 
 
@@ -134,22 +139,48 @@ def workload(args, rank, world=1):
     return datagen.make("sift", args.n, seed=1, part=rank, components=1000)
 
 
+def host_info() -> dict:
+    """CPU model and core count of the host the oracle runs on."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
 def cpu_baseline(args, X) -> dict:
-    """The oracle as it stands, single thread, on a bounded sample of the
-    same workload: the first `cpu_sample` rows, same k/p/iters/seed; build
-    seconds extrapolated linearly in n (GNND's per-iteration work is
-    per-node: sample, 2p-bounded join, bounded update)."""
+    """The oracle as it stands, single thread pinned to core 0 (the
+    process affinity is set to {0} around the call: `taskset -c 0`), on a
+    bounded sample of the same workload: the first `cpu_sample` rows, same
+    k/p/iters/seed; build seconds extrapolated linearly in n (GNND's
+    per-iteration work is per-node: sample, 2p-bounded join, bounded
+    update).  A full-size oracle build of C2 is tools/oracle_full_c2.py."""
     import oracle.oracle as orc
     ns = min(args.cpu_sample, X.shape[0])
     Xs = np.ascontiguousarray(X[:ns])
-    t0 = time.perf_counter()
-    orc.build(Xs, args.k, args.p, args.iters, args.seed)
-    dt = time.perf_counter() - t0
+    old = None
+    try:
+        old = os.sched_getaffinity(0)
+        os.sched_setaffinity(0, {0})
+    except Exception:
+        old = None
+    try:
+        t0 = time.perf_counter()
+        orc.build(Xs, args.k, args.p, args.iters, args.seed)
+        dt = time.perf_counter() - t0
+    finally:
+        if old is not None:
+            os.sched_setaffinity(0, old)
+    info = host_info()
     return {"value": dt * (X.shape[0] / ns), "unit": "s", "cores": 1, "kind": "oracle",
             "sample": f"oracle GNND build of the first {ns} rows of the same SIFT1M-shaped workload "
-                      f"(k={args.k}, p={args.p}, iters={args.iters}) took {dt:.2f} s on 1 host core; "
-                      f"value = that x {X.shape[0]}/{ns} (linear in n)",
-            "sample_seconds": dt}
+                      f"(k={args.k}, p={args.p}, iters={args.iters}) took {dt:.2f} s on 1 host core (affinity "
+                      f"{{0}}); value = that x {X.shape[0]}/{ns} (linear in n)",
+            "pinned_core": 0 if old is not None else None, **info, "sample_seconds": dt}
 
 
 def run_reference(args):
@@ -253,6 +284,81 @@ def measure_ggm(args, K, Xd, stream):
             "dist_evals": sum(s["dist_evals"] for s in st), "accepted": sum(s["accepted"] for s in st),
             "dist_evals_per_s": sum(s["dist_evals"] for s in st) / (ms * 1e-3),
             "kernel_ms_per_merge": kernels}
+
+
+FP32_ISSUE_PEAK = None  # set from the SM count and the sampled clock
+
+
+def measure_deep(args, K, stream, clk_ghz):
+    """The metric's second shape: DEEP-shaped continuous fp32 rows (d = 96,
+    L2-normalised GMM-LR, 10^4 components; BASELINE.json configs[3] shape)
+    at the largest direct single-GPU size the bench budget allows, built with
+    knng_build (the float path: k_join_ws, no exact-u8 shortcut).  Device
+    time with CUDA events; recall@10 on 10k sampled nodes vs brute force."""
+    import torch
+
+    import datagen
+    n, d = args.deep_rows, 96
+    X = datagen.make_device("deep", n, seed=2)
+    torch.cuda.synchronize()
+    ws = torch.empty(K.knng_build_workspace_bytes(K.KNNG_F32, n, d, args.k, args.p), dtype=torch.uint8, device="cuda")
+    ids = torch.empty((n, args.k), dtype=torch.int32, device="cuda")
+    dists = torch.empty((n, args.k), dtype=torch.float32, device="cuda")
+
+    def step():
+        K.knng_build(X, args.k, args.deep_iters, args.p, args.seed, "l2", ids, dists, ws, stream)
+
+    for _ in range(max(1, args.deep_warmup)):
+        step()
+    torch.cuda.synchronize()
+    K.knng_set_timing(True)
+    K.knng_reset_timing()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    hist = []
+    for _ in range(args.deep_steps):
+        step()
+        hist.extend(K.knng_last_stats())
+    e1.record(stream)
+    torch.cuda.synchronize()
+    K.knng_set_timing(False)
+    ms = e0.elapsed_time(e1) / args.deep_steps
+    exact_u8 = bool(K.knng_get_option("last_exact_u8"))
+    join_ms, join_launches = K.knng_kernel_time("k_join")
+    kernels = {}
+    for nm in ["k_init", "k_merge_sample", "k_scan_reduce", "k_rev_scatter", "k_rev_select", "k_join", "k_merge",
+               "k_export"]:
+        t, c = K.knng_kernel_time(nm)
+        if c:
+            kernels[nm] = round(t / args.deep_steps, 3)
+    rec, nq = recall_at_10(K, X, dists, args.recall_nodes, ids)
+    evals = sum(s["dist_evals"] for s in hist)
+    rows = sum(s["rows"] for s in hist)
+    L = max(1, join_launches)
+    join_avg = join_ms / L
+    # ALU roofline of the canonical fp32 tile (D5): FADD + FFMA per dimension
+    # and pair, against the FP32 pipe (148 SMs x 128 lanes x clock)
+    fp_instr = evals * d * 2 / L
+    fp_peak = 148 * 128 * clk_ghz * 1e9
+    achieved = fp_instr / (join_avg * 1e-3)
+    hbm_peak, _ = peaks()
+    gbs = rows * (d * 4 + 4) / L / (join_avg * 1e-3) / 1e9
+    return {"workload": f"DEEP-shaped {n} x {d} continuous fp32 (BASELINE.json configs[3] row shape; GMM-LR "
+                        f"10^4 components, L2-normalised, generated on the GPU), direct knng_build on one B200",
+            "metric": METRIC, "value": ms / 1000.0, "unit": "s", "ms_per_step": ms, "steps": args.deep_steps,
+            "warmup": max(1, args.deep_warmup), "higher_is_better": False, "dtype": "u8" if exact_u8 else "f32",
+            "config": {"n": n, "d": d, "k": args.k, "sample_size": args.p, "iters": args.deep_iters, "metric": "l2",
+                       "l2_flush": f"inputs ({n * d * 4 / 1e9:.1f} GB) larger than L2"},
+            "recall_at_10": rec, "recall_nodes": nq,
+            "roofline": {"bound": "alu", "kernel": "k_join (k_join_ws, canonical fp32 tile)",
+                         "achieved": achieved / 1e9, "peak": fp_peak / 1e9, "unit": "G fp32-instr/s",
+                         "frac": achieved / fp_peak, "instr_per_dim_pair": 2, "sm_clock_ghz": clk_ghz,
+                         "avg_launch_ms": join_avg, "launches": join_launches,
+                         "share_of_step": join_ms / args.deep_steps / ms if ms > 0 else None,
+                         "hbm_view": {"achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
+                                      "alg_bytes_per_launch": rows * (d * 4 + 4) / L}},
+            "throughput": {"dist_evals_per_s": evals / args.deep_steps / (ms * 1e-3)},
+            "kernel_ms_per_build": kernels}
 
 
 def main():
@@ -415,10 +521,13 @@ def main():
                "api": "knng_build_host" if world == 1 else "knng_build_sharded over NCCL (per-rank H2D/D2H)"}
 
     # ---- roofline of the dominant kernel (k_join), DESIGN.md section 6:
-    # HBM view: algorithmic gather bytes = rows x (d x element + 4 id bytes);
-    # ALU view: the canonical tile's minimum instruction count -- f32: FADD +
-    # FFMA per dim and pair; exact-u8: VABSDIFF4 + IDP4A per 4 dims and pair
-    # -- against the SM issue peak (148 SMs x 4 warp-instr/cycle x clock).
+    # HBM view (primary): algorithmic gather bytes = rows x (d x element + 4
+    # id bytes) per launch / launch time.  Tensor view (the exact-u8 tile is
+    # an int8 Gram matrix on tcgen05): the method's int8 multiply-adds,
+    # dist_evals x d x 2 ops, against the int8 dense peak (the measured bf16
+    # burst peak x 2, the guide's nominal int8:bf16 ratio).  Issue view: the
+    # measured issue-active fraction of the same kernel from the committed
+    # ncu capture (profiles/join_traffic.json).
     esz = 1 if exact_u8 else 4
     rows = sum(s["rows"] for s in history)
     evals = sum(s["dist_evals"] for s in history)
@@ -428,33 +537,51 @@ def main():
     join_avg_ms = join_ms / launches_in_hist
     achieved_gbs = alg_bytes_per_launch / (join_avg_ms * 1e-3) / 1e9 if join_avg_ms > 0 else 0.0
     peak, peak_kind = peaks()
-    instr_per_dim_pair = 0.5 if exact_u8 else 2.0
-    warp_instr = evals * d * instr_per_dim_pair / 32 / launches_in_hist
     clk_ghz = (clk.get("sm_mhz") or 1965.0) / 1000.0
-    issue_peak = 148 * 4 * clk_ghz * 1e9
-    issue_rate = warp_instr / (join_avg_ms * 1e-3) if join_avg_ms > 0 else 0.0
-    traffic = None
+    traffic, ncu_issue = None, None
     try:  # dram__bytes_read.sum + dram__bytes_write.sum of one ncu --set full capture
         with open(os.path.join(ROOT, "profiles", "join_traffic.json")) as f:
             tj = json.load(f)
         traffic = tj.get("u8" if exact_u8 else "f32")
+        ncu_issue = tj.get("issue_active_u8" if exact_u8 else "issue_active_f32")
     except Exception:
         pass
-    alu = {"bound": "alu", "achieved": issue_rate / 1e9, "peak": issue_peak / 1e9,
-           "unit": "G warp-instr/s", "frac": issue_rate / issue_peak,
-           "instr_per_dim_pair": instr_per_dim_pair, "sm_clock_ghz": clk_ghz}
+    views = {}
+    if exact_u8:
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+                bf16 = float(json.load(f)["bf16_tflops"])
+            i8_src = "measured bf16 burst x 2"
+        except Exception:
+            bf16, i8_src = 2250.0, "nominal bf16 2250 TF/s x 2 (fallback)"
+        ops = evals * d * 2 / launches_in_hist
+        tops = ops / (join_avg_ms * 1e-3) / 1e12 if join_avg_ms > 0 else 0.0
+        views["tensor"] = {"bound": "tensor", "achieved": tops, "peak": 2 * bf16, "unit": "TOPS int8",
+                           "frac": tops / (2 * bf16), "peak_source": i8_src,
+                           "note": "method's multiply-adds only; the 128x128 Gram tile computes ~8x more"}
+    else:
+        fp_instr = evals * d * 2 / launches_in_hist
+        ach = fp_instr / (join_avg_ms * 1e-3) if join_avg_ms > 0 else 0.0
+        fpk = 148 * 128 * clk_ghz * 1e9
+        views["alu"] = {"bound": "alu", "achieved": ach / 1e9, "peak": fpk / 1e9, "unit": "G fp32-instr/s",
+                        "frac": ach / fpk, "instr_per_dim_pair": 2}
+    if ncu_issue is not None:
+        views["issue"] = {"issue_active": ncu_issue, "source": "profiles/join_traffic.json (ncu --set full)"}
     roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
                 "frac": achieved_gbs / peak, "traffic": traffic, "peak_source": peak_kind,
                 "kernel": "k_join", "avg_launch_ms": join_avg_ms, "launches": join_launches,
                 "share_of_step": join_ms / args.steps / ms if ms > 0 else None,
-                "alg_bytes_per_launch": alg_bytes_per_launch, "element_bytes": esz,
-                "alu": alu}
+                "alg_bytes_per_launch": alg_bytes_per_launch, "element_bytes": esz, "views": views}
     throughput = {"dist_evals_per_s": evals / args.steps / (ms * 1e-3),
                   "accepted_updates_per_s": accepted / args.steps / (ms * 1e-3), "per": "rank 0"}
 
     ggm = None
     if world == 1 and not args.no_ggm:
         ggm = measure_ggm(args, K, Xd, stream)
+
+    deep = None
+    if world == 1 and args.deep_rows > 0:
+        deep = measure_deep(args, K, stream, clk_ghz)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -481,7 +608,8 @@ def main():
                         + ("; built on the exact uint8 path (option exact_u8: graph bit-identical to fp32)"
                            if exact_u8 else ""),
                 "config": cfg, "recall_at_10": recall, "recall_nodes": nq,
-                "roofline": roofline, "throughput": throughput, "ggm": ggm, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": roofline, "throughput": throughput, "ggm": ggm, "shapes": {"deep": deep},
+                "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clk, "iter_stats": stats}
         print(json.dumps(line), flush=True)
     if world > 1:

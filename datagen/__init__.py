@@ -96,3 +96,36 @@ def sample_nodes(n: int, count: int, seed: int = 6) -> np.ndarray:
     rng = np.random.default_rng(seed)
     count = min(count, n)
     return np.sort(rng.choice(n, size=count, replace=False)).astype(np.int64)
+
+
+def make_device(shape: str, n: int, seed: int = 1, device="cuda", components: int | None = None,
+                chunk: int = 1 << 20):
+    """The same GMM-LR recipe generated on the GPU with torch (float32, a
+    torch.Generator stream): for bench workloads whose host generation would
+    take minutes (DEEP-shaped 10^7-10^8 rows).  Same distribution and
+    post-processing as make(); not the same numbers (the host recipe is the
+    bit-reproducible one the oracle-side tests use)."""
+    import torch
+    d, C, r, sc, sa, sn = SHAPES[shape]
+    C = components or min(C, max(1, n // 8))
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed))
+    mu = torch.randn((C, d), generator=g, device=device) * sc
+    At = torch.randn((C, r, d), generator=g, device=device) * (sa / float(np.sqrt(r)))
+    out = torch.empty((n, d), dtype=torch.float32, device=device)
+    for lo in range(0, n, chunk):
+        hi = min(n, lo + chunk)
+        m = hi - lo
+        lab = torch.randint(0, C, (m,), generator=g, device=device)
+        z = torch.randn((m, r), generator=g, device=device)
+        x = mu[lab] + torch.randn((m, d), generator=g, device=device) * sn
+        for j in range(r):  # x += A_c z, one latent coordinate at a time
+            x += At[lab, j, :] * z[:, j:j + 1]
+        if shape == "sift":
+            x = torch.clamp(torch.round(32.0 + 24.0 * x), 0.0, 255.0)
+        elif shape == "gist":
+            x = torch.clamp(0.25 + 0.08 * x, min=0.0)
+        elif shape == "deep":
+            x = x / torch.linalg.vector_norm(x, dim=1, keepdim=True)
+        out[lo:hi] = x
+    return out
