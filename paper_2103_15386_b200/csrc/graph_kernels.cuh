@@ -143,71 +143,55 @@ __global__ void __launch_bounds__(256, 8) k_merge_sample(Dims D, Graph G, Sample
     if (do_merge) {
         const uint32_t c = G.bcnt[s];
         if (c > 0) {
-            extern __shared__ uint64_t ms_scratch[];  // 64 u64 per warp: scratch, list copy
-            uint64_t* scr = ms_scratch + (threadIdx.x >> 5) * 64;
-            uint64_t* lst = scr + 32;
+            extern __shared__ uint64_t ms_scratch[];  // per warp: list copy, merged keys (64 u64), metas (32 u32)
+            uint64_t* lst = ms_scratch + (threadIdx.x >> 5) * 80;
+            uint64_t* outk = lst + 32;
+            uint32_t* outm = reinterpret_cast<uint32_t*>(lst + 64);
             const uint64_t* bk = G.bucket + G.boff[s];
             for (uint32_t base = 0; base < c; base += 32) {
                 const uint64_t cand = (base + lane < c) ? bk[base + lane] : kSentinel;
                 // Pre-filter (exact): a candidate equal to a list key is the
                 // same id (D5 keys are canonical per id) and one not below the
-                // current k-th key cannot enter the k smallest.  Only the
-                // survivors go through the sorting network.
+                // current k-th key cannot enter the k smallest.
                 const uint64_t kth = shfl_u64(cur.key, k - 1);
                 __syncwarp();
                 lst[lane] = cur.key;
                 __syncwarp();
-                int pos = 0;
+                int pos = 0;  // list entries below cand
 #pragma unroll
                 for (int step = 16; step > 0; step >>= 1)
                     if (lst[pos + step - 1] < cand) pos += step;
-                const bool keep = cand < kth && lst[pos] != cand;
+                bool keep = cand < kth && lst[pos] != cand;
+                // repeated candidates (the same key from two joins): the lowest lane stays
+                const uint32_t km0 = __ballot_sync(kFull, keep);
+                if (km0 == 0) continue;
+                const uint32_t same = __match_any_sync(kFull, keep ? cand : kSentinel);
+                keep = keep && (same & km0 & lanemask_lt()) == 0u;
                 const uint32_t km = __ballot_sync(kFull, keep);
-                if (km == 0) continue;
-                const int cnt = __popc(km);
-                if (cnt <= 4) {
-                    // few survivors: insert them one by one (position by
-                    // ballot, shift by one lane) instead of a sorting network
-                    uint32_t rem = km;
-                    while (rem) {
-                        const int src = __ffs(rem) - 1;
-                        rem &= rem - 1;
-                        const uint64_t x = shfl_u64(cand, src);
-                        if (__any_sync(kFull, cur.key == x)) continue;  // repeated candidate
-                        const int pos = __popc(__ballot_sync(kFull, cur.key < x));
-                        const uint64_t up = shfl_u64(cur.key, lane > 0 ? lane - 1 : 0);
-                        const uint32_t upm = __shfl_sync(kFull, cur.meta, lane > 0 ? lane - 1 : 0);
-                        if (static_cast<int>(lane) > pos) {
-                            cur.key = up;
-                            cur.meta = upm;
-                        } else if (static_cast<int>(lane) == pos) {
-                            cur.key = x;
-                            cur.meta = 3u;  // NEW, from a bucket
-                        }
-                    }
-                    continue;
+                // Merge by ranks (no sorting network): a survivor lands at
+                // (list entries below it) + (survivors below it); a list entry
+                // moves down by the survivors below it; past slot k: dropped.
+                int r = 0, sh = 0;
+                for (uint32_t rem = km; rem; rem &= rem - 1) {
+                    const uint64_t x = shfl_u64(cand, __ffs(rem) - 1);
+                    r += x < cand;
+                    sh += x < cur.key;
                 }
                 __syncwarp();
-                scr[lane] = kSentinel;
+                outk[lane] = kSentinel;
+                outm[lane] = 0u;
                 __syncwarp();
-                if (keep) scr[__popc(km & lanemask_lt())] = (cand << 1) | 1ull;
-                __syncwarp();
-                // sort the survivors (network sized to their count), drop
-                // repeated candidates, merge with the list
-                const int P = cnt <= 2 ? 2 : cnt <= 4 ? 4 : cnt <= 8 ? 8 : cnt <= 16 ? 16 : 32;
-                uint64_t y = warp_sort_u64_blocks(scr[lane], P);
-                const uint64_t prev = shfl_u64(y, (lane + 31) & 31);
-                const bool uniq = y != kSentinel && (lane == 0 || y != prev);
-                const uint32_t um = __ballot_sync(kFull, uniq);
-                if (__popc(um) != cnt) {  // repeats present: re-compact
-                    __syncwarp();
-                    scr[lane] = kSentinel;
-                    __syncwarp();
-                    if (uniq) scr[__popc(um & lanemask_lt())] = y;
-                    __syncwarp();
-                    y = scr[lane];
+                if (in_list && static_cast<int>(lane) + sh < k) {
+                    outk[lane + sh] = cur.key;
+                    outm[lane + sh] = cur.meta;
                 }
-                warp_merge_list_disjoint(cur.key, cur.meta, y);
+                if (keep && pos + r < k) {
+                    outk[pos + r] = cand;
+                    outm[pos + r] = 3u;  // NEW, from a bucket
+                }
+                __syncwarp();
+                cur.key = outk[lane];
+                cur.meta = outm[lane];
             }
             changed = true;
             if (!in_list) cur = Elem{kSentinel, 0u};

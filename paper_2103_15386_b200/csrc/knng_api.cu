@@ -446,7 +446,7 @@ struct Run {
             if (sg == 2) k_merge_sample_seg<2><<<grid, wpb * 32, sm, c.stream>>>(D, G, S, do_merge, do_sample, ps);
             else if (sg == 3) k_merge_sample_seg<3><<<grid, wpb * 32, sm, c.stream>>>(D, G, S, do_merge, do_sample, ps);
             else if (sg == 4) k_merge_sample_seg<4><<<grid, wpb * 32, sm, c.stream>>>(D, G, S, do_merge, do_sample, ps);
-            else k_merge_sample<<<grid, wpb * 32, wpb * 64 * sizeof(uint64_t), c.stream>>>(D, G, S, do_merge, do_sample, ps);
+            else k_merge_sample<<<grid, wpb * 32, wpb * 80 * sizeof(uint64_t), c.stream>>>(D, G, S, do_merge, do_sample, ps);
         });
     }
 
