@@ -2,6 +2,10 @@
 NVCC      ?= nvcc
 ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := -O3 -std=c++17 $(ARCH) -lineinfo --fmad=false -Xcompiler -fPIC,-Wall -shared -ldl
+NVFLAGS   += $(NVEXTRA)
+ifeq ($(WSPROF),1)
+NVFLAGS   += -DKNNG_WS_PROF
+endif
 PKG       := paper_2103_15386_b200
 LIB       := $(PKG)/lib/libknng.so
 SRCS      := $(wildcard $(PKG)/csrc/*.cu $(PKG)/csrc/*.cuh) include/knng.h

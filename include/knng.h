@@ -270,7 +270,11 @@ knng_status knng_debug_philox(const uint32_t* ctr, int64_t m, uint64_t seed,
  *                  CUDA-core join (join_ws.cuh);
  *                  1: the batched cp.async join (join_kernel.cuh; also the
  *                     automatic choice for rows that are not 16-B aligned);
- *                  2: always the warp-specialised join;
+ *                  2: always the warp-specialised join (float rows: the
+ *                     packed FP32x2 tile, FADD2/FFMA2 on pair-interleaved
+ *                     stages);
+ *                  3: the warp-specialised join with the scalar FP32 tile
+ *                     (the previous float path, kept as the A/B reference);
  *                  4: float rows (L2 / cosine, d % 4 == 0, d <= 128): the
  *                     TF32 tensor-core join (join_tcf.cuh) -- exact
  *                     selection by canonical recomputation inside an

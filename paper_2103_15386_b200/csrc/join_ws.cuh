@@ -62,6 +62,10 @@ struct WsMeta {
     int m[kWsMaxNodes], q[kWsMaxNodes], sbase[kWsMaxNodes], bbase[kWsMaxNodes + 1];
     int obase[kWsMaxNodes + 1];  // prefix of the 2m+q selected keys per node
     uint32_t ids[kWsSlots];
+    // node (index in the batch) of every 4x4 block and of every selected
+    // key: one shared load instead of a dependent search over the prefixes
+    uint8_t bnode[kWsBlocks];
+    uint8_t onode[2 * kWsSlots];
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -101,6 +105,60 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
         ns = ns < 512 ? ns * 2 : 512;
     }
 }
+// Idle wait of the roles with slack (gather, lead, epilogue) in the packed
+// join: test once, then plain nanosleep back-off (not woken by barrier
+// traffic).  Every test is a shared-memory barrier operation competing with
+// the consumers' LDS.  (try_wait with a suspend-time hint compiles to
+// TRYWAIT + NANOSLEEP.SYNCS, which every arrive in the CTA wakes: under ncu
+// SYNCS + NANOSLEEP + BRA were 46 % of the kernel's instructions.)
+#ifndef WS_IDLE_MAX_NS
+#define WS_IDLE_MAX_NS 1024
+#endif
+#ifndef WS_IDLE_MIN_NS
+#define WS_IDLE_MIN_NS 64
+#endif
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return done != 0;
+}
+__device__ __forceinline__ void mbar_wait_idle(uint64_t* bar, uint32_t parity) {
+    uint32_t ns = WS_IDLE_MIN_NS;
+    while (!mbar_test(bar, parity)) {
+        __nanosleep(ns);
+        ns = ns < WS_IDLE_MAX_NS ? 2 * ns : WS_IDLE_MAX_NS;
+    }
+}
+// Packed FP32x2 steps of the canonical accumulation (D5/D6) for two pairs
+// (a, b0) and (a, b1) at once: b = {b0_i, b1_i}, acc = {acc0, acc1}.  Both
+// lanes are IEEE round-to-nearest sub and fused multiply-add, i.e. exactly
+// t = a_i - b_i; acc = fmaf(t, t, acc) of each pair (FADD2 / FFMA2 on
+// sm_100a, the scalar a broadcast by the .F32 operand selector).
+__device__ __forceinline__ unsigned long long f2_l2(float a, unsigned long long b, unsigned long long acc) {
+    unsigned long long r;
+    asm("{\n\t.reg .b64 aa, tt;\n\tmov.b64 aa, {%1, %1};\n\tsub.rn.f32x2 tt, aa, %2;\n\t"
+        "fma.rn.f32x2 %0, tt, tt, %3;\n\t}"
+        : "=l"(r)
+        : "f"(a), "l"(b), "l"(acc));
+    return r;
+}
+// acc = fmaf(a_i, b_i, acc) for two pairs (cosine on normalised rows, D6)
+__device__ __forceinline__ unsigned long long f2_ip(float a, unsigned long long b, unsigned long long acc) {
+    unsigned long long r;
+    asm("{\n\t.reg .b64 aa;\n\tmov.b64 aa, {%1, %1};\n\tfma.rn.f32x2 %0, aa, %2, %3;\n\t}"
+        : "=l"(r)
+        : "f"(a), "l"(b), "l"(acc));
+    return r;
+}
+__device__ __forceinline__ float f2_lo(unsigned long long v) { return __uint_as_float(static_cast<uint32_t>(v)); }
+__device__ __forceinline__ float f2_hi(unsigned long long v) { return __uint_as_float(static_cast<uint32_t>(v >> 32)); }
+
 __device__ __forceinline__ void named_bar(int id, int threads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
@@ -123,18 +181,30 @@ __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* tm, in
 
 
 
-template <typename T, int MET, int STAGES>
+template <typename T, int MET, int STAGES, bool PK = false>
 struct WsCfg {
     using E = typename std::conditional<MET == kMetCos, float, T>::type;
     static constexpr int SD = SlabCfg<T>::kDims;
-    // 128-B row slabs (32 f32 or 128 u8 dims) whose 16-B chunks are
-    // XOR-swizzled by (slot >> 2) & 7, so the LDS.128 of lanes on different
-    // 4-row groups never share a bank group (padding cannot: rows 4 apart
-    // always collide).
+    // PK (float rows): the pair-interleaved stage of the packed FP32x2 tile.
+    // Slots 2j and 2j+1 share one 256-B "pair row" whose 16-B chunk c holds
+    // {s0[2c], s1[2c], s0[2c+1], s1[2c+1]} of the 32-dim slab, so one
+    // LDS.128 yields two packed column pairs {b0_i, b1_i} (FADD2/FFMA2
+    // operands) or four row scalars.  Chunk c sits at position
+    // ((c & 1) << 3) | (c >> 1) (even chunks in the first 128 B: the
+    // gather's 8-lane phases write distinct bank groups), and 4-slot groups
+    // are 528 B apart (16-B pad), so blocks of different 4-row groups read
+    // different bank groups without any address swizzle.
+    static constexpr bool kPair = PK && std::is_same<E, float>::value;
+    static constexpr int kGroupFloats = 132;  // 2 pair rows of 64 floats + 4 pad
+    // otherwise: 128-B row slabs (32 f32 or 128 u8 dims) whose 16-B chunks
+    // are XOR-swizzled by (slot >> 2) & 7, so the LDS.128 of lanes on
+    // different 4-row groups never share a bank group (padding cannot: rows
+    // 4 apart always collide).
     static constexpr bool kSwz = true;
     static constexpr int RS = SD;
     static_assert(SD * sizeof(E) == 128, "row slabs are 128 B");
-    static constexpr size_t kStageBytes = sizeof(E) * kWsSlots * RS;
+    static constexpr size_t kStageBytes =
+        kPair ? sizeof(float) * kGroupFloats * (kWsSlots / 4) : sizeof(E) * kWsSlots * RS;
     static constexpr size_t kMetaOff = kStageBytes * STAGES;
     static constexpr size_t kPartOff = (kMetaOff + sizeof(WsMeta) * kWsMeta + 15) & ~size_t(15);
     static constexpr size_t kPartBytes = sizeof(unsigned long long) * 8 * kWsBlocks;  // row + col minima
@@ -149,11 +219,43 @@ struct WsCfg {
     static_assert(kSmem + 1024 <= 232448, "227 KB dynamic shared memory per CTA (+ 1 KB TMA alignment)");
 };
 
-template <typename T, int MET, int STAGES>
+#ifdef KNNG_WS_PROF
+// profiling build only (make WSPROF=1; tools/join_probe.py): role probes
+// (1 consumers skip the math, 2 gathers skip the loads, 4 no filing) and
+// cycles spent per wait site (probe bit 32)
+__device__ int g_ws_probe;
+__device__ unsigned long long g_ws_prof[32];
+#define WS_PROBE() (*(volatile int*)&g_ws_probe)
+#define WS_T0(v) const long long v = clock64()
+#define WS_ACC(v, site)                                                                         \
+    do {                                                                                        \
+        if ((WS_PROBE() & 32) && (threadIdx.x & 31) == 0)                                       \
+            atomicAdd(&g_ws_prof[site], static_cast<unsigned long long>(clock64() - (v)));      \
+    } while (0)
+#else
+#define WS_PROBE() 0
+#define WS_T0(v)
+#define WS_ACC(v, site)
+#endif
+
+template <bool SUSP>
+__device__ __forceinline__ void ws_idle_wait(uint64_t* bar, uint32_t parity, int site = 31) {
+#ifdef KNNG_WS_PROF
+    const long long t0 = clock64();
+#endif
+    if constexpr (SUSP) mbar_wait_idle(bar, parity);
+    else mbar_wait_sleep(bar, parity);
+#ifdef KNNG_WS_PROF
+    if ((WS_PROBE() & 32) && (threadIdx.x & 31) == 0)
+        atomicAdd(&g_ws_prof[site], static_cast<unsigned long long>(clock64() - t0));
+#endif
+}
+
+template <typename T, int MET, int STAGES, bool PK = false>
 __global__ void __launch_bounds__(kWsThreads, 1)
 k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G, Samples S, int64_t boundary,
           unsigned long long* __restrict__ work, DevStats* __restrict__ stats) {
-    using Cfg = WsCfg<T, MET, STAGES>;
+    using Cfg = WsCfg<T, MET, STAGES, PK>;
     using E = typename Cfg::E;
     constexpr bool kFloat = std::is_same<E, float>::value;
     using Acc = typename std::conditional<kFloat, float, unsigned int>::type;
@@ -181,10 +283,14 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
     const int d = D.d, cap = D.cap;
     const int nslab = (d + SD - 1) / SD;
     const bool restricted = boundary >= 0;
+    const int probe = WS_PROBE();
 
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(full + s, kWsProdThreads);  // one cp.async arrive per gather thread
+            // non-packed: one cp.async arrive per gather thread; packed: one
+            // arrive per gather warp (each arrive wakes the CTA's suspended
+            // waiters: 224 per slab made the idle roles spin)
+            mbar_init(full + s, Cfg::kPair ? kWsGatherWarps : kWsProdThreads);
             mbar_init(empty + s, kWsConsumerWarps);
         }
         for (int s = 0; s < kWsMeta; ++s) {
@@ -214,11 +320,12 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
         unsigned long long n_cand = 0, n_app = 0;
         for (uint32_t b = g;; b += kWsEpiGroups) {
             const int mb = b % kWsMeta, pb = b & 1;
-            mbar_wait_sleep(mfull + mb, (b / kWsMeta) & 1);
+            ws_idle_wait<Cfg::kPair>(mfull + mb, (b / kWsMeta) & 1, 0);
             const WsMeta& M = meta[mb];
             const int nn = M.nnodes;
             if (nn == 0) break;
-            mbar_wait_sleep(pfull + pb, (b >> 1) & 1);
+            ws_idle_wait<Cfg::kPair>(pfull + pb, (b >> 1) & 1, 1);
+            WS_T0(t_sel);
             const unsigned long long* rowp = parts + pb * 8 * kWsBlocks;
             const unsigned long long* colp = rowp + 4 * kWsBlocks;
             // output o of the batch is key j of node i (obase[i] <= o): c_nn(u_j)
@@ -229,8 +336,7 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
                 uint64_t v = kSentinel;
                 uint32_t tgt = 0;
                 if (o < total) {
-                    int i = 0;
-                    while (i + 1 < nn && M.obase[i + 1] <= o) ++i;
+                    const int i = M.onode[o];
                     const int j = o - M.obase[i];
                     const int mi = M.m[i], qi = M.q[i];
                     const int mgi = (mi + 3) >> 2, qgi = (qi + 3) >> 2, bb = M.bbase[i];
@@ -268,11 +374,13 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
             }
             // partials and metadata are no longer needed: release them so the
             // consumers and the lead producer run ahead of the filing
+            WS_ACC(t_sel, 12);
             named_bar(2 + g, kWsEpiThreads);
             if (et == 0) {
                 mbar_arrive(pempty + pb);
                 mbar_arrive(mempty + mb);
             }
+            WS_T0(t_file);
             // file the keys into their targets' buckets (the k_cand_scatter
             // step, fused); keys >= the target's iteration-start k-th key
             // cannot enter (exact, D17).  All loads, then all atomics, then
@@ -309,6 +417,7 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
                 }
                 continue;
             }
+            if (probe & 4) continue;
 #pragma unroll
             for (int r = 0; r < kEpiRounds; ++r) {
                 n_cand += kv[r] != kSentinel;
@@ -319,6 +428,7 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
 #pragma unroll
             for (int r = 0; r < kEpiRounds; ++r)
                 if (sl[r] != 0xFFFFFFFFu) G.bucket[bo[r] + sl[r]] = kv[r];
+            WS_ACC(t_file, 13);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -343,11 +453,56 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
         constexpr int kRowsPerPass = kWsProdThreads / CPR;
         const int part = ptid % CPR;
         const int row0 = ptid / CPR;
+        // packed layout: each task is (pair row j, 16-B column c4 of the
+        // slab): two LDG.128 (slots 2j, 2j+1, dims 4c4..4c4+3), interleaved
+        // in registers into chunks 2c4 and 2c4+1 (two STS.128).  All of a
+        // slab's loads are issued before the stage is awaited, then stored,
+        // then the stage's full barrier is arrived on (release: the stores
+        // are visible to the consumers that observe the phase).
+        constexpr int kTaskPerThr = (kWsSlots / 2 * 8 + kWsProdThreads - 1) / kWsProdThreads;
+        auto gather_pk = [&](const WsMeta& M) {
+            const int npairs = M.nslots >> 1;
+            for (int sl = 0; sl < nslab; ++sl) {
+                const int st = slab_it % STAGES;
+                const int ncol = min(SD, d - sl * SD) >> 2;  // 16-B columns in this slab (d % 4 == 0)
+                float4 r0[kTaskPerThr], r1[kTaskPerThr];
+#pragma unroll
+                for (int i = 0; i < kTaskPerThr; ++i) {
+                    const int task = ptid + i * kWsProdThreads, j = task >> 3, c4 = task & 7;
+                    r0[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    r1[i] = r0[i];
+                    if (j < npairs && c4 < ncol && !(probe & 2)) {
+                        const uint32_t i0 = M.ids[2 * j], i1 = M.ids[2 * j + 1];
+                        const E* src = V + sl * SD + 4 * c4;
+                        if (i0 != 0xFFFFFFFFu) r0[i] = __ldg(reinterpret_cast<const float4*>(src + static_cast<size_t>(i0) * d));
+                        if (i1 != 0xFFFFFFFFu) r1[i] = __ldg(reinterpret_cast<const float4*>(src + static_cast<size_t>(i1) * d));
+                    }
+                }
+                ws_idle_wait<Cfg::kPair>(empty + st, ((slab_it / STAGES) & 1) ^ 1, 2);
+                float* stage = reinterpret_cast<float*>(ring) + static_cast<size_t>(st) * (Cfg::kStageBytes / 4);
+#pragma unroll
+                for (int i = 0; i < kTaskPerThr; ++i) {
+                    const int task = ptid + i * kWsProdThreads, j = task >> 3, c4 = task & 7;
+                    if (j < npairs && c4 < ncol) {
+                        float* row = stage + (j >> 1) * Cfg::kGroupFloats + (j & 1) * 64;
+                        *reinterpret_cast<float4*>(row + 4 * c4) = make_float4(r0[i].x, r1[i].x, r0[i].y, r1[i].y);
+                        *reinterpret_cast<float4*>(row + 32 + 4 * c4) = make_float4(r0[i].z, r1[i].z, r0[i].w, r1[i].w);
+                    }
+                }
+                __syncwarp();  // the warp's stores before its one release arrive
+                if (lane == 0) mbar_arrive(full + st);
+                ++slab_it;
+            }
+        };
         auto gather = [&](const WsMeta& M) {
+            if constexpr (Cfg::kPair) {
+                gather_pk(M);
+                return;
+            }
             const int nslots = M.nslots;
             for (int sl = 0; sl < nslab; ++sl) {
                 const int st = slab_it % STAGES;
-                mbar_wait_sleep(empty + st, ((slab_it / STAGES) & 1) ^ 1);
+                ws_idle_wait<Cfg::kPair>(empty + st, ((slab_it / STAGES) & 1) ^ 1, 3);
                 const int e0 = sl * SD + part * CE;
                 E* dst = ring + static_cast<size_t>(st) * kWsSlots * RS;
                 const E* src0 = V + e0;
@@ -377,7 +532,7 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
         if (warp < kWsConsumerWarps + kWsGatherWarps) {  // gather warps follow the batch stream
             while (true) {
                 const int mb = meta_it % kWsMeta;
-                mbar_wait_sleep(mfull + mb, (meta_it / kWsMeta) & 1);
+                ws_idle_wait<Cfg::kPair>(mfull + mb, (meta_it / kWsMeta) & 1, 4);
                 const WsMeta& M = meta[mb];
                 if (M.nnodes == 0) break;
                 gather(M);
@@ -412,13 +567,29 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
                                  "l"(S.gcnt + 2 * xb + lo), "r"(bytes)
                                  : "memory");
                 }
-                for (int e = lane; e < nodes * 2 * cap; e += 32) {
-                    const int node = e / (2 * cap), w = e - node * 2 * cap;
-                    const uint32_t* src = w < cap ? S.G + static_cast<size_t>(xb + node) * cap + w
-                                                  : S.G + static_cast<size_t>(D.n) * cap +
-                                                        static_cast<size_t>(xb + node) * cap + (w - cap);
-                    const uint32_t s = smem_u32(cids + e);
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(src) : "memory");
+                if ((cap & 3) == 0) {
+                    // 16-B copies, node-major: lane -> (node of the pass, chunk of its Gn|Go rows)
+                    const int cpr = cap >> 2, per_node = 2 * cpr, npi = 32 / per_node;
+                    const int sub = static_cast<int>(lane) / per_node, c = static_cast<int>(lane) - sub * per_node;
+                    const uint32_t* base = (c < cpr ? S.G : S.G + static_cast<size_t>(D.n) * cap) + 4 * (c < cpr ? c : c - cpr);
+                    for (int nb = 0; nb < nodes; nb += npi) {
+                        const int node = nb + sub;
+                        if (sub < npi && node < nodes) {
+                            const uint32_t s = smem_u32(cids + node * 2 * cap + 4 * c);
+                            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s),
+                                         "l"(base + static_cast<size_t>(xb + node) * cap)
+                                         : "memory");
+                        }
+                    }
+                } else {
+                    for (int node = 0; node < nodes; ++node)
+                        for (int w = lane; w < 2 * cap; w += 32) {
+                            const uint32_t* src = w < cap ? S.G + static_cast<size_t>(xb + node) * cap + w
+                                                          : S.G + static_cast<size_t>(D.n) * cap +
+                                                                static_cast<size_t>(xb + node) * cap + (w - cap);
+                            const uint32_t s = smem_u32(cids + node * 2 * cap + w);
+                            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(src) : "memory");
+                        }
                 }
             }
             cp_async_commit();
@@ -433,6 +604,7 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
         while (true) {
             if (cur >= 32) {
                 if (x0 >= D.n) break;
+                WS_T0(t_chunk);
                 const unsigned long long claimed = claim();  // used one chunk later
                 fetch(buf ^ 1, xnext);
                 cp_async_wait<1>();  // this chunk's group has landed
@@ -454,6 +626,7 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
                 x0 = xnext;
                 xnext = static_cast<int64_t>(__shfl_sync(kFull, claimed, 0));
                 buf ^= 1;
+                WS_ACC(t_chunk, 11);
             }
             // take nodes cur.. while the batch's blocks and slots fit
             const bool pending = static_cast<int>(lane) >= cur;
@@ -473,8 +646,9 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
             if (nb_tot == 0) continue;  // only nodes without NEW samples
             // ---- publish batch metadata
             const int mb = meta_it % kWsMeta;
-            mbar_wait_sleep(mempty + mb, ((meta_it / kWsMeta) & 1) ^ 1);
+            ws_idle_wait<Cfg::kPair>(mempty + mb, ((meta_it / kWsMeta) & 1) ^ 1, 5);
             WsMeta& M = meta[mb];
+            WS_T0(t_pub);
             const int nn = end - first;
             const int excl_b = cb - (pending ? my_nb : 0), excl_s = cs - (pending ? my_sl : 0);
             const bool in_batch = static_cast<int>(lane) >= first && static_cast<int>(lane) < end;
@@ -506,20 +680,29 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
                 M.bbase[nn] = nb_tot;
                 M.obase[nn] = no_tot;
             }
-            __syncwarp();  // node table visible to the whole warp
-            // sample ids of every slot of the batch, from the chunk cache
+            // node by node (values broadcast from the node's lane): the sample
+            // ids of its slots from the chunk cache, and its index in the
+            // block -> node and key -> node tables
             const uint32_t* cids = cc_ids + static_cast<size_t>(cur_buf) * 32 * 2 * cap;
-            for (int j = lane; j < ns_tot; j += 32) {
-                int i = 0;
-                while (i + 1 < nn && M.sbase[i + 1] <= j) ++i;
-                const int m = M.m[i], q = M.q[i], mpad = (m + 3) & ~3, js = j - M.sbase[i];
-                const uint32_t* row = cids + (first + i) * 2 * cap;
-                uint32_t id = 0xFFFFFFFFu;
-                if (js < m) id = row[js];
-                else if (js >= mpad && js - mpad < q) id = row[cap + (js - mpad)];
-                M.ids[j] = id;
+            const int my_ob = co - (2 * my_m + my_q);
+            for (int i = 0; i < nn; ++i) {
+                const int src = first + i;
+                const int m = __shfl_sync(kFull, my_m, src), q = __shfl_sync(kFull, my_q, src);
+                const int sb = __shfl_sync(kFull, excl_s, src), bb = __shfl_sync(kFull, excl_b, src);
+                const int ob = __shfl_sync(kFull, my_ob, src);
+                const int mpad = (m + 3) & ~3, mg = mpad >> 2, qg = (q + 3) >> 2;
+                const uint32_t* row = cids + src * 2 * cap;
+                for (int js = lane; js < 4 * (mg + qg); js += 32) {
+                    uint32_t id = 0xFFFFFFFFu;
+                    if (js < m) id = row[js];
+                    else if (js >= mpad && js - mpad < q) id = row[cap + (js - mpad)];
+                    M.ids[sb + js] = id;
+                }
+                for (int t = lane; t < mg * (mg + 1) / 2 + mg * qg; t += 32) M.bnode[bb + t] = static_cast<uint8_t>(i);
+                for (int o = lane; o < 2 * m + q; o += 32) M.onode[ob + o] = static_cast<uint8_t>(i);
             }
             __syncwarp();
+            WS_ACC(t_pub, 10);
             mbar_arrive(mfull + mb);  // all 32 lanes: releases every lane's writes
             ++meta_it;
         }
@@ -528,7 +711,7 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
         // its own batch sequence); consumers and gatherers stop at the first
         for (int e = 0; e < kWsEpiGroups; ++e) {
             const int mb = meta_it % kWsMeta;
-            mbar_wait_sleep(mempty + mb, ((meta_it / kWsMeta) & 1) ^ 1);
+            ws_idle_wait<Cfg::kPair>(mempty + mb, ((meta_it / kWsMeta) & 1) ^ 1, 6);
             if (lane == 0) meta[mb].nnodes = 0;
             __syncwarp();
             mbar_arrive(mfull + mb);
@@ -555,15 +738,14 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
     unsigned long long my_pairs = 0;
     for (uint32_t b = 0;; ++b) {
         const int mb = b % kWsMeta, pb = b & 1;
-        mbar_wait_sleep(mfull + mb, (b / kWsMeta) & 1);
+        if constexpr (Cfg::kPair) mbar_wait(mfull + mb, (b / kWsMeta) & 1);  // the critical role spins
+        else ws_idle_wait<false>(mfull + mb, (b / kWsMeta) & 1, 7);
         const WsMeta& M = meta[mb];
         const int nn = M.nnodes;
         if (nn == 0) break;
         // ---- my block
         const bool active = ct < M.nblocks;
-        int nd = 0;
-        if (active)
-            while (nd + 1 < nn && M.bbase[nd + 1] <= ct) ++nd;
+        const int nd = active ? M.bnode[ct] : 0;
         const int m = M.m[nd], q = M.q[nd], sb = M.sbase[nd];
         const int mpad = (m + 3) & ~3, mg = mpad >> 2, qg = (q + 3) >> 2;
         const int t = ct - M.bbase[nd];
@@ -593,11 +775,53 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
         for (int r = 0; r < 4; ++r)
 #pragma unroll
             for (int c = 0; c < 4; ++c) acc[r][c] = Acc(0);
+        // packed accumulators: acc2[r][h] = {acc[r][2h], acc[r][2h+1]}
+        unsigned long long acc2[4][2];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc2[r][0] = acc2[r][1] = 0ull;
 
         for (int sl = 0; sl < nslab; ++sl) {
             const int st = slab_it % STAGES;
             mbar_wait(full + st, (slab_it / STAGES) & 1);
-            if (active) {
+            WS_T0(t_slab);
+            if constexpr (Cfg::kPair) {
+                if (active && !(probe & 1)) {
+                    // rows rb..rb+3 and columns cb..cb+3 are 4-slot groups
+                    const float* stage = reinterpret_cast<const float*>(ring) + static_cast<size_t>(st) * (Cfg::kStageBytes / 4);
+                    const float* A = stage + ((sb + rb) >> 2) * Cfg::kGroupFloats;
+                    const float* B = stage + ((sb + cb) >> 2) * Cfg::kGroupFloats;
+                    const int nc = min(SD, d - sl * SD) >> 1;  // 2-dim chunks, in dimension order
+#pragma unroll
+                    for (int c = 0; c < SD / 2; ++c) {
+                        if (c >= nc) break;
+                        const int pos = (((c & 1) << 3) | (c >> 1)) * 4;
+                        const float4 a01 = *reinterpret_cast<const float4*>(A + pos);       // r0,r1 @2c; r0,r1 @2c+1
+                        const float4 a23 = *reinterpret_cast<const float4*>(A + 64 + pos);  // r2,r3
+                        const ulonglong2 b01 = *reinterpret_cast<const ulonglong2*>(B + pos);       // {c0,c1} @2c, @2c+1
+                        const ulonglong2 b23 = *reinterpret_cast<const ulonglong2*>(B + 64 + pos);  // {c2,c3}
+                        const float ar[2][4] = {{a01.x, a01.y, a23.x, a23.y}, {a01.z, a01.w, a23.z, a23.w}};
+                        const unsigned long long bp[2][2] = {{b01.x, b23.x}, {b01.y, b23.y}};
+#pragma unroll
+                        for (int h = 0; h < 2; ++h)
+#pragma unroll
+                            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                                for (int cp = 0; cp < 2; ++cp) {
+                                    if constexpr (MET == kMetCos) {
+                                        acc2[r][cp] = f2_ip(ar[h][r], bp[h][cp], acc2[r][cp]);
+                                    } else if constexpr (MET == kMetChi2) {
+                                        float lo = f2_lo(acc2[r][cp]), hi = f2_hi(acc2[r][cp]);
+                                        lo = chi2_term(ar[h][r], f2_lo(bp[h][cp]), lo);
+                                        hi = chi2_term(ar[h][r], f2_hi(bp[h][cp]), hi);
+                                        acc2[r][cp] = (static_cast<unsigned long long>(__float_as_uint(hi)) << 32) |
+                                                      __float_as_uint(lo);
+                                    } else {
+                                        acc2[r][cp] = f2_l2(ar[h][r], bp[h][cp], acc2[r][cp]);
+                                    }
+                                }
+                    }
+                }
+            } else if (active) {
                 const E* __restrict__ A = ring + static_cast<size_t>(st) * kWsSlots * RS + aoff;
                 const E* __restrict__ B = ring + static_cast<size_t>(st) * kWsSlots * RS + boff;
                 const int lim = min(SD, d - sl * SD);
@@ -659,14 +883,25 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
                     }
                 }
             }
+            WS_ACC(t_slab, 14);
             __syncwarp();
             if (lane == 0) mbar_arrive(empty + st);
             ++slab_it;
         }
-
+        WS_T0(t_min);
+        if constexpr (Cfg::kPair) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int cp = 0; cp < 2; ++cp) {
+                    acc[r][2 * cp] = f2_lo(acc2[r][cp]);
+                    acc[r][2 * cp + 1] = f2_hi(acc2[r][cp]);
+                }
+        }
         // ---- block minima: 4 row keys (c_nn / c_no candidates of the NEW
         // rows) and 4 column keys (c_nn / c_on candidates of the columns)
-        mbar_wait_sleep(pempty + pb, ((b >> 1) & 1) ^ 1);
+        if constexpr (Cfg::kPair) mbar_wait(pempty + pb, ((b >> 1) & 1) ^ 1);
+        else ws_idle_wait<false>(pempty + pb, ((b >> 1) & 1) ^ 1, 8);
         unsigned long long* rowp = parts + pb * 8 * kWsBlocks;
         unsigned long long* colp = rowp + 4 * kWsBlocks;
         if (active) {
@@ -708,6 +943,7 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
             for (int c = 0; c < 4; ++c) colp[ct * 4 + c] = colbest[c];
         }
         __syncwarp();
+        WS_ACC(t_min, 15);
         if (lane == 0) mbar_arrive(pfull + pb);
     }
 #pragma unroll

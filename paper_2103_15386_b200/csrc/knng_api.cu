@@ -619,29 +619,28 @@ struct Run {
         if (al && !force_v3) {
             // warp-specialised pipeline (bulk row copies need 16-B aligned,
             // 16-B multiple row slabs)
-            constexpr int STG = 5;
+            constexpr int STG = 4;   // 32-KB stages (row-slab layout: u8, option 3)
+            constexpr int STP = 4;   // 33-KB stages (pair-interleaved layout of the packed FP32x2 tile)
+            const bool pk = jk != 3;  // option 3: the scalar FP32 tile (A/B reference point)
             unsigned long long* work = reinterpret_cast<unsigned long long*>(ws + L.flag + 8);
             cudaMemsetAsync(work, 0, 8, c.stream);
+            const float* Xf = static_cast<const float*>(X);
+            auto go = [&](auto kfn, size_t sm, auto Xp, const float* Xnp) {
+                cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+                kfn<<<sms, kWsThreads, sm, c.stream>>>(Xp, Xnp, D, G, S, boundary, work, st);
+            };
             c.launch("k_join", [&] {
                 if (metric == KNNG_COSINE) {
-                    constexpr size_t sm = WsCfg<float, true, STG>::kSmem;
-                    cudaFuncSetAttribute(k_join_ws<float, true, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-                    k_join_ws<float, true, STG><<<sms, kWsThreads, sm, c.stream>>>(nullptr, Xn, D, G, S, boundary, work, st);
+                    if (pk) go(k_join_ws<float, kMetCos, STP, true>, WsCfg<float, kMetCos, STP, true>::kSmem, Xf, Xn);
+                    else go(k_join_ws<float, kMetCos, STG, false>, WsCfg<float, kMetCos, STG, false>::kSmem, Xf, Xn);
                 } else if (metric == KNNG_CHI2) {
-                    constexpr size_t sm = WsCfg<float, kMetChi2, STG>::kSmem;
-                    cudaFuncSetAttribute(k_join_ws<float, kMetChi2, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-                    k_join_ws<float, kMetChi2, STG><<<sms, kWsThreads, sm, c.stream>>>(static_cast<const float*>(X), nullptr,
-                                                                                       D, G, S, boundary, work, st);
+                    go(k_join_ws<float, kMetChi2, STP, true>, WsCfg<float, kMetChi2, STP, true>::kSmem, Xf, nullptr);
                 } else if (dt == KNNG_F32) {
-                    constexpr size_t sm = WsCfg<float, false, STG>::kSmem;
-                    cudaFuncSetAttribute(k_join_ws<float, false, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-                    k_join_ws<float, false, STG><<<sms, kWsThreads, sm, c.stream>>>(static_cast<const float*>(X), nullptr,
-                                                                                    D, G, S, boundary, work, st);
+                    if (pk) go(k_join_ws<float, kMetL2, STP, true>, WsCfg<float, kMetL2, STP, true>::kSmem, Xf, nullptr);
+                    else go(k_join_ws<float, kMetL2, STG, false>, WsCfg<float, kMetL2, STG, false>::kSmem, Xf, nullptr);
                 } else {
-                    constexpr size_t sm = WsCfg<uint8_t, false, STG>::kSmem;
-                    cudaFuncSetAttribute(k_join_ws<uint8_t, false, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-                    k_join_ws<uint8_t, false, STG><<<sms, kWsThreads, sm, c.stream>>>(static_cast<const uint8_t*>(X), nullptr,
-                                                                                      D, G, S, boundary, work, st);
+                    go(k_join_ws<uint8_t, kMetL2, STG, false>, WsCfg<uint8_t, kMetL2, STG, false>::kSmem,
+                       static_cast<const uint8_t*>(X), nullptr);
                 }
             });
             return true;
@@ -1302,8 +1301,17 @@ knng_status knng_set_option(const char* name, int64_t value) {
         g_opt_update.store(static_cast<int>(value));
         return KNNG_OK;
     }
+#ifdef KNNG_WS_PROF
+    if (strcmp(name, "ws_probe") == 0) {  // profiling build only
+        const int v = static_cast<int>(value);
+        cudaMemcpyToSymbol(g_ws_probe, &v, sizeof(int));
+        unsigned long long z[32] = {};
+        cudaMemcpyToSymbol(g_ws_prof, z, sizeof(z));
+        return KNNG_OK;
+    }
+#endif
     if (strcmp(name, "join_kernel") == 0) {
-        if (value < 0 || value > 4 || value == 3) return fail(KNNG_E_USAGE, "join_kernel must be 0, 1, 2 or 4");
+        if (value < 0 || value > 4) return fail(KNNG_E_USAGE, "join_kernel must be 0..4");
         g_opt_join_kernel.store(static_cast<int>(value));
         return KNNG_OK;
     }
@@ -1316,6 +1324,13 @@ knng_status knng_get_option(const char* name, int64_t* host_value) {
     else if (strcmp(name, "join_kernel") == 0) *host_value = g_opt_join_kernel.load();
     else if (strcmp(name, "update") == 0) *host_value = g_opt_update.load();
     else if (strcmp(name, "last_exact_u8") == 0) *host_value = g_last_exact_u8;
+#ifdef KNNG_WS_PROF
+    else if (strncmp(name, "ws_prof", 7) == 0) {  // profiling build only
+        unsigned long long v[32];
+        cudaMemcpyFromSymbol(v, g_ws_prof, sizeof(v));
+        *host_value = static_cast<int64_t>(v[atoi(name + 7)]);
+    }
+#endif
     else return fail(KNNG_E_USAGE, "unknown option '%s'", name);
     return KNNG_OK;
 }

@@ -240,7 +240,7 @@ def test_legacy_join_kernel_matches(K):
         K.knng_set_option("join_kernel", 0)
 
 
-@pytest.mark.parametrize("jk", [0, 4])
+@pytest.mark.parametrize("jk", [0, 3, 4])
 @pytest.mark.parametrize("shape,d,metric", [("deep", 96, "l2"), ("deep", 96, "cosine"), ("gist", 128, "l2"),
                                             ("c1", 32, "l2"), ("gist", 60, "cosine")])
 def test_join_kernels_f32_match(K, jk, shape, d, metric):

@@ -19,12 +19,10 @@ ap.add_argument("--p", type=int, default=16)
 ap.add_argument("--iters", type=int, default=7)
 ap.add_argument("--metric", default="l2")
 ap.add_argument("--opts", default="0,2")
-ap.add_argument("--orders", default="0", help="join_order values to try with every option")
 a = ap.parse_args()
-X = torch.from_numpy(datagen.make(a.shape, a.n, seed=1, d=a.d)).cuda()
-for o, jo in [(o, jo) for o in a.opts.split(",") for jo in a.orders.split(",")]:
+X = (torch.from_numpy(datagen.make(a.shape, a.n, seed=1, d=a.d)) if a.n <= 2_000_000 else datagen.make_device(a.shape, a.n, seed=1)).cuda()
+for o in a.opts.split(","):
     K.knng_set_option("join_kernel", int(o))
-    K.knng_set_option("join_order", int(jo))
     K.knng_build(X, a.k, a.iters, a.p, 42, a.metric)
     K.knng_set_timing(True)
     K.knng_reset_timing()
@@ -32,8 +30,7 @@ for o, jo in [(o, jo) for o in a.opts.split(",") for jo in a.orders.split(",")]:
     K.knng_set_timing(False)
     ms, n = K.knng_kernel_time("k_join")
     st = K.knng_last_stats()
-    print(f"{a.shape} d={X.shape[1]} {a.metric} join_kernel={o} join_order={jo}: k_join {ms / max(n, 1):.3f} ms/launch over {n}; "
+    print(f"{a.shape} d={X.shape[1]} {a.metric} join_kernel={o}: k_join {ms / max(n, 1):.3f} ms/launch over {n}; "
           f"recomputed/candidates {sum(s['recomputed'] for s in st) / max(1, sum(s['candidates'] for s in st)):.2f}",
           flush=True)
 K.knng_set_option("join_kernel", 0)
-K.knng_set_option("join_order", 0)

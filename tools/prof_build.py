@@ -22,15 +22,22 @@ ap.add_argument("--k", type=int, default=32)
 ap.add_argument("--p", type=int, default=16)
 ap.add_argument("--iters", type=int, default=8)
 ap.add_argument("--builds", type=int, default=1)
+ap.add_argument("--shape", default="sift")
+ap.add_argument("--metric", default="l2")
+ap.add_argument("--join-kernel", type=int, default=0)
 a = ap.parse_args()
-cache = f"/tmp/sift_{a.n}.npy"  # datagen takes ~25 s per 1M rows; reuse within one box session
-if os.path.exists(cache):
-    Xh = np.load(cache)
+if a.shape == "sift":
+    cache = f"/tmp/sift_{a.n}.npy"  # datagen takes ~25 s per 1M rows; reuse within one box session
+    if os.path.exists(cache):
+        Xh = np.load(cache)
+    else:
+        Xh = datagen.make("sift", a.n, seed=1)
+        np.save(cache, Xh)
+    X = torch.from_numpy(Xh).cuda()
 else:
-    Xh = datagen.make("sift", a.n, seed=1)
-    np.save(cache, Xh)
-X = torch.from_numpy(Xh).cuda()
+    X = datagen.make_device(a.shape, a.n, seed=1)
+K.knng_set_option("join_kernel", a.join_kernel)
 for _ in range(a.builds):
-    K.knng_build(X, a.k, a.iters, a.p, 42)
+    K.knng_build(X, a.k, a.iters, a.p, 42, a.metric)
 torch.cuda.synchronize()
 print("stats", K.knng_last_stats())
