@@ -133,7 +133,10 @@ __device__ __forceinline__ uint32_t bit_range(int a, int b) {
 // then keep 24 epilogue warps resident instead of 16.
 // TMA: rows gathered by tcgen05-era TMA gather4 (one instruction per 4 rows,
 // issued by warp 0) instead of 16-B cp.async copies by every thread.
-template <int EPI, int CTAS, bool TMA>
+// REC: record mode of the distributed refine (dist_kernels.cuh) -- a template
+// parameter, so the single-GPU build carries no per-key mode branch (the
+// runtime check cost ~10 % of this kernel: 2.47 -> 2.73 ms per C2 launch).
+template <int EPI, int CTAS, bool TMA, bool REC>
 __global__ void __launch_bounds__((EPI + 1) * 32, CTAS)
 k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Graph G, Samples S, int64_t boundary,
           unsigned long long* __restrict__ work, DevStats* __restrict__ stats,
@@ -350,7 +353,7 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
 #pragma unroll
         for (int r = 0; r < 2; ++r)
             if (f2_key[r] != kSentinel) {
-                if (G.rec_cnt) {  // record mode (distributed refine)
+                if constexpr (REC) {  // record mode (distributed refine)
                     G.rec_key[f2_pos[r]] = f2_key[r];
                     G.rec_tgt[f2_pos[r]] = f2_tgt;
                 } else {
@@ -362,7 +365,7 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
         const bool ok0 = f1_key[0] < f1_th, ok1 = f1_key[1] < f1_th;  // D17 (the sentinel never passes)
         n_app += ok0 + ok1;
         uint64_t sl = 0;
-        if (G.rec_cnt) {
+        if constexpr (REC) {
             // record slots: one atomic per warp (the call is warp-uniform)
             const uint32_t b0 = __ballot_sync(kFull, ok0), b1 = __ballot_sync(kFull, ok1);
             unsigned long long wb = 0;
@@ -526,18 +529,29 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
                 B &= 0xFFFFu;
                 if (isNEW) my_pairs += __popc(A & bit_range(0, s - cb)) + __popc(B);
                 const int4* nv4 = reinterpret_cast<const int4*>(nb + cb);
+                int kk[16];
 #pragma unroll
                 for (int g = 0; g < 4; ++g) {
                     const int4 n4 = nv4[g];
-                    const int kk[4] = {n4.x - static_cast<int>(r[4 * g] << 8),
-                                       n4.y - static_cast<int>(r[4 * g + 1] << 8),
-                                       n4.z - static_cast<int>(r[4 * g + 2] << 8),
-                                       n4.w - static_cast<int>(r[4 * g + 3] << 8)};
+                    kk[4 * g] = n4.x - static_cast<int>(r[4 * g] << 8);
+                    kk[4 * g + 1] = n4.y - static_cast<int>(r[4 * g + 1] << 8);
+                    kk[4 * g + 2] = n4.z - static_cast<int>(r[4 * g + 2] << 8);
+                    kk[4 * g + 3] = n4.w - static_cast<int>(r[4 * g + 3] << 8);
+                }
+                // masked minima, 3-input VIMNMX3; a mask that is empty on
+                // every lane of the warp (OLD rows, chunks outside the OLD
+                // range) is skipped as a whole
+                if (__any_sync(kFull, A != 0u)) {
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        if ((A >> (4 * g + e)) & 1u) minA = min(minA, kk[e]);
-                        if ((B >> (4 * g + e)) & 1u) minB = min(minB, kk[e]);
-                    }
+                    for (int e = 0; e < 16; e += 2)
+                        minA = __vimin3_s32(minA, (A >> e) & 1u ? kk[e] : INT_MAX,
+                                            (A >> (e + 1)) & 1u ? kk[e + 1] : INT_MAX);
+                }
+                if (__any_sync(kFull, B != 0u)) {
+#pragma unroll
+                    for (int e = 0; e < 16; e += 2)
+                        minB = __vimin3_s32(minB, (B >> e) & 1u ? kk[e] : INT_MAX,
+                                            (B >> (e + 1)) & 1u ? kk[e + 1] : INT_MAX);
                 }
             }
             tc_fence_before();
@@ -565,7 +579,7 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
             n_cand += (k1 != kSentinel) + (k2 != kSentinel);
             if (k1 != kSentinel || k2 != kSentinel) {  // D15: (inf, inf) inserts nothing
                 f1_th = __ldg(G.kth_t + my_id);
-                if (!G.rec_cnt) f1_bo = __ldg(G.boff + my_id);
+                if constexpr (!REC) f1_bo = __ldg(G.boff + my_id);
             }
             // batch b+1's norms (their loads were issued one iteration ago);
             // buffer (b+1) % 3 was last read by the scans of b-2

@@ -570,13 +570,15 @@ struct Run {
                 // rows by TMA gather4; 16-B cp.async copies if the driver's
                 // tensor-map encoder is unavailable (bit-identical)
                 const bool tma = make_row_tmap(X, xr, D.d, &tm);
-                auto go = [&](auto kfn, int ctas, int threads) {
+                const bool rec = G.rec_cnt != nullptr;  // record mode: the distributed refine
+                auto go = [&](auto kfn) {
                     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-                    kfn<<<ctas * sms, threads, sm, c.stream>>>(static_cast<const uint8_t*>(X), sqn, D, G, S, boundary,
-                                                               work, st, tm);
+                    kfn<<<3 * sms, 9 * 32, sm, c.stream>>>(static_cast<const uint8_t*>(X), sqn, D, G, S, boundary,
+                                                          work, st, tm);
                 };
-                if (tma) go(k_join_tc<8, 3, true>, 3, 9 * 32);  // 8 epilogue warps, 3 CTAs per SM
-                else go(k_join_tc<8, 3, false>, 3, 9 * 32);
+                // 8 epilogue warps, 3 CTAs per SM
+                if (tma) rec ? go(k_join_tc<8, 3, true, true>) : go(k_join_tc<8, 3, true, false>);
+                else rec ? go(k_join_tc<8, 3, false, true>) : go(k_join_tc<8, 3, false, false>);
             });
             return true;
         }
