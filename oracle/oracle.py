@@ -325,3 +325,52 @@ def extend(X_old, keys_old, X_new, k, p, iters, merge_iters, seed, metric=L2SQ):
     ids, dists = build(X_new, k, p, iters, seed, metric)
     keys_in = np.concatenate([keys_old, key(dists, ids.astype(np.uint64) + np.uint64(n_old))])
     return merge(np.concatenate([X_old, X_new]), keys_in, n_old, k, p, merge_iters, seed, 0, metric)
+
+
+def shard_bounds(n: int, shards: int) -> list:
+    """Contiguous shard g = rows [g n / S, (g+1) n / S) ("partitioned
+    into multiple shards")."""
+    return [g * n // shards for g in range(shards + 1)]
+
+
+def allpairs_level(i: int, h: int, shards: int) -> int:
+    """Philox level word of the merge of shards i < h (D41): i * S + h."""
+    return i * shards + h
+
+
+def allpairs_build(X, shards, k, p, iters, merge_iters, seed, metric=L2SQ, order=None):
+    """The paper's out-of-memory scheme (D41): GNND builds the
+    sub-graph G_g of every shard g (seed + g, local ids); then GGM merges
+    every pair of sub-graphs (i < h) once -- Alg. 3 on S_i U S_h with A = G_i,
+    B = G_h, Philox level i * S + h -- and "each k-NN list in either
+    sub-graph retains the top-k neighbors": the merged lists are folded into
+    the running lists R of both shards (R(x) <- k smallest unique keys of
+    R(x) U M(x), InsertIntoNNList per entry, D17).  R starts as the shards'
+    own graphs with global ids.  `order`: the sequence of pairs (default
+    (0,1), (0,2), ..., (S-2,S-1)); the result does not depend on it.
+    Returns keys [n, k] with global ids."""
+    X = _c(X)
+    n = X.shape[0]
+    b = shard_bounds(n, shards)
+    G, R = [], np.zeros((n, k), np.uint64)
+    for g in range(shards):
+        ids, dists = build(X[b[g]:b[g + 1]], k, p, iters, seed + g, metric)
+        G.append(key(dists, ids))
+        R[b[g]:b[g + 1]] = key(dists, ids.astype(np.uint64) + np.uint64(b[g]))
+    pairs = order if order is not None else [(i, h) for i in range(shards) for h in range(i + 1, shards)]
+    flags = np.zeros(k, np.uint8)
+    for i, h in pairs:
+        nA = b[i + 1] - b[i]
+        Xp = np.concatenate([X[b[i]:b[i + 1]], X[b[h]:b[h + 1]]])
+        keys_in = np.concatenate([G[i], key(key_dists(G[h]), key_ids(G[h]).astype(np.uint64) + np.uint64(nA))])
+        M = merge(Xp, keys_in, nA, k, p, merge_iters, seed, allpairs_level(i, h, shards), metric)
+        mid = key_ids(M).astype(np.int64)
+        gid = np.where(mid < nA, mid + b[i], mid - nA + b[h]).astype(np.uint64)
+        Mg = key(key_dists(M), gid)
+        rows = list(range(b[i], b[i + 1])) + list(range(b[h], b[h + 1]))
+        for r, x in enumerate(rows):
+            lst = R[x].copy()
+            for kk in Mg[r]:
+                list_insert(lst, flags, int(kk))
+            R[x] = lst
+    return R
