@@ -151,6 +151,31 @@ knng_status knng_extend(const void* vec_old, int64_t n_old, const uint32_t* ids_
                         uint64_t seed, uint32_t* out_ids, float* out_dists, void* stream);
 
 /* ------------------------------------------------------------------------
+ * knng_build_ooc -- the paper's out-of-memory construction (P:298-302,
+ * DESIGN.md D41): "the large-scale dataset is partitioned into multiple
+ * shards ... a k-NN graph for each shard is built by GNND and saved back to
+ * disk.  GGM is called to merge every two sub-graphs of two shards ... Each
+ * k-NN list in either sub-graphs retains the top-k neighbors".
+ *   Shard g = rows [g n / S, (g+1) n / S).  GNND per shard (seed + g); GGM
+ *   of every pair i < h once (merge_iters refine iterations, Philox level
+ *   i * S + h, seed); the merged lists of both shards are folded into their
+ *   running lists (k smallest unique keys).  Only one resident shard and two
+ *   streamed shards live on the GPU: host buffers play the disk, and the
+ *   transfers of the next pair overlap the current merge (a copy stream).
+ *   host_vectors [n][d] HOST (pageable, pinned or mmap'ed); host_out_ids /
+ *   host_out_dists [n][k] HOST, global ids, each list ascending.
+ *   The library allocates device memory for 3 shards + one merge workspace
+ *   and pinned host memory for the sub-graphs and running lists (3 n k x 4 B).
+ *   Requires k <= 32, every shard > k rows, 1 <= shards <= 181.  Blocks
+ *   until done.  Bit-identical to oracle.allpairs_build.  knng_last_stats:
+ *   the shard builds' iterations, then every merge's.
+ * ---------------------------------------------------------------------- */
+knng_status knng_build_ooc(const void* host_vectors, knng_dtype dt, int64_t n, int32_t d, int32_t k,
+                           knng_metric metric, int32_t iters, int32_t merge_iters, int32_t sample_size,
+                           uint64_t seed, int32_t shards, uint32_t* host_out_ids, float* host_out_dists,
+                           void* stream);
+
+/* ------------------------------------------------------------------------
  * Multi-GPU (one process -- or one host thread -- per GPU).
  * The paper builds sub-graphs of the shards on different GPUs and merges
  * them with GGM ("GGM allows the k-NN graph to be built on multiple

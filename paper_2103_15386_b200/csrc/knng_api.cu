@@ -1340,3 +1340,6 @@ knng_status knng_get_option(const char* name, int64_t* host_value) {
 int32_t knng_abi_version(void) { return 2; }
 
 }  // extern "C"
+
+// the out-of-memory all-pairs construction: host orchestration
+#include "ooc_api.cuh"

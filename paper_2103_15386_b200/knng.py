@@ -57,6 +57,7 @@ SIGNATURES = [
     ("knng_comm_destroy", i32, [P]),
     ("knng_build_sharded", i32, [P, P, i64, i64, i64, i32, i32, i32, i32, i32, i32, P, i32, u64, P, P, P]),
     ("knng_bruteforce", i32, [P, i32, i64, i32, i32, P, i64, i32, P, P, P]),
+    ("knng_build_ooc", i32, [P, i32, i64, i32, i32, i32, i32, i32, i32, u64, i32, P, P, P]),
     ("knng_debug_init", i32, [P, i32, i64, i32, i32, i32, u64, P, P, P]),
     ("knng_debug_iterate", i32, [P, i32, i64, i32, i32, i32, i32, u32, u64, i64, P, P, P, P, sz, P]),
     ("knng_debug_sample", i32, [i64, i32, i32, u32, u64, P, P, P, P, P, P, P, sz, P]),
@@ -165,6 +166,21 @@ def knng_build_host(vectors: np.ndarray, k: int, iters: int, sample_size: int, s
         out_dists = np.empty((n, k), np.float32)
     _check(lib().knng_build_host(_ptr(vectors), _dtype_code(vectors), n, d, k, _metric(metric), iters,
                                  sample_size, seed, _ptr(out_ids), _ptr(out_dists), _stream(stream)))
+    return out_ids, out_dists
+
+
+def knng_build_ooc(vectors: np.ndarray, k: int, iters: int, merge_iters: int, sample_size: int, shards: int,
+                   seed: int = 0, metric="l2", out_ids=None, out_dists=None, stream=None):
+    """The paper's out-of-memory construction from HOST buffers:
+    GNND per shard, GGM of every pair of sub-graphs, running top-k lists."""
+    assert vectors.flags.c_contiguous and vectors.ndim == 2
+    n, d = vectors.shape
+    if out_ids is None:
+        out_ids = np.empty((n, k), np.uint32)
+    if out_dists is None:
+        out_dists = np.empty((n, k), np.float32)
+    _check(lib().knng_build_ooc(_ptr(vectors), _dtype_code(vectors), n, d, k, _metric(metric), iters, merge_iters,
+                                sample_size, seed, shards, _ptr(out_ids), _ptr(out_dists), _stream(stream)))
     return out_ids, out_dists
 
 
