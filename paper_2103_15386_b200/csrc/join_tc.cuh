@@ -174,7 +174,7 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
     unsigned long long claimed = 0;
     int my_m = 0, my_q = 0;
     bool more = true;
-    unsigned long long n_joins = 0, n_m = 0, n_q = 0;
+    unsigned long long n_joins = 0, n_m = 0, n_q = 0, n_rows = 0;  // n_rows: sample rows staged
     auto claim = [&]() -> unsigned long long {
         unsigned long long c0 = 0;
         if (lane == 0) c0 = atomicAdd(work, 32ull);
@@ -230,6 +230,27 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
             my_q = cc_cnt[cbuf * 64 + 2 * lane + 1];
         }
         if (my_m == 0) my_q = 0;
+        if (my_m > 0) {  // the join counters keep the method's m and q
+            ++n_joins;
+            n_m += my_m;
+            n_q += my_q;
+        }
+        if (restricted && my_m > 0) {
+            // GGM refine (D22): every NEW sample is cross-subset, so the only
+            // pairs left are (NEW, OLD in x's own subset); OLD samples of the
+            // other subset meet nothing.  Keep only the own-subset OLD ids
+            // (in place, id order kept) -- fewer rows staged and scanned, and
+            // a node without any is skipped.  Same candidates, same counts.
+            uint32_t* orow = cc_ids + static_cast<size_t>(cbuf) * 32 * 2 * cap + lane * 2 * cap + cap;
+            const bool xs = D.base + xnext + static_cast<int64_t>(lane) >= boundary;
+            int qq = 0;
+            for (int j = 0; j < my_q; ++j) {
+                const uint32_t id = orow[j];
+                if ((static_cast<int64_t>(id) >= boundary) == xs) orow[qq++] = id;
+            }
+            my_q = qq;
+            if (qq == 0) my_m = 0;
+        }
         pend = __ballot_sync(kFull, my_m > 0);
         xnext = static_cast<int64_t>(__shfl_sync(kFull, claimed, 0));
         claimed = claim();
@@ -258,9 +279,7 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
                 P.sb[nn] = ns_used;
                 P.m[nn] = m;
                 P.q[nn] = q;
-                ++n_joins;
-                n_m += m;
-                n_q += q;
+                n_rows += m + q;
             }
             const uint32_t* row = cids + L * 2 * cap;
             for (int js = lane; js < m + q; js += 32) {
@@ -614,6 +633,7 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
         n_joins += __shfl_xor_sync(kFull, n_joins, o);
         n_m += __shfl_xor_sync(kFull, n_m, o);
         n_q += __shfl_xor_sync(kFull, n_q, o);
+        n_rows += __shfl_xor_sync(kFull, n_rows, o);
     }
     if (lane == 0) {
         if (n_cand) atomicAdd(&stats->candidates, n_cand);
@@ -623,7 +643,7 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
             atomicAdd(&stats->joins, n_joins);
             atomicAdd(&stats->sum_m, n_m);
             atomicAdd(&stats->sum_q, n_q);
-            atomicAdd(&stats->rows, n_m + n_q);
+            atomicAdd(&stats->rows, n_rows);
         }
     }
 }

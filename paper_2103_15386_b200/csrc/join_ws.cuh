@@ -600,7 +600,7 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
         fetch(0, x0);
         int cur = 32;  // position inside the current 32-node chunk
         int my_m = 0, my_q = 0, my_nb = 0, my_sl = 0;
-        unsigned long long n_joins = 0, n_m = 0, n_q = 0;
+        unsigned long long n_joins = 0, n_m = 0, n_q = 0, n_rows = 0;
         while (true) {
             if (cur >= 32) {
                 if (x0 >= D.n) break;
@@ -617,6 +617,26 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
                     my_q = cc_cnt[buf * 64 + 2 * lane + 1];
                 }
                 if (my_m == 0) my_q = 0;  // no NEW sample: nothing to join
+                if (my_m > 0) {  // the join counters keep the method's m and q
+                    ++n_joins;
+                    n_m += my_m;
+                    n_q += my_q;
+                }
+                if (restricted && my_m > 0) {
+                    // GGM refine (D22): NEW samples are all cross-subset, so
+                    // only (NEW, own-subset OLD) pairs remain; keep the
+                    // own-subset OLD ids in place (id order kept), skip a node
+                    // without any.  Same candidates and counts, fewer rows.
+                    uint32_t* orow = cc_ids + static_cast<size_t>(buf) * 32 * 2 * cap + lane * 2 * cap + cap;
+                    const bool xs = D.base + x >= boundary;
+                    int qq = 0;
+                    for (int j = 0; j < my_q; ++j) {
+                        const uint32_t id = orow[j];
+                        if ((static_cast<int64_t>(id) >= boundary) == xs) orow[qq++] = id;
+                    }
+                    my_q = qq;
+                    if (qq == 0) my_m = 0;
+                }
                 const int mg = (my_m + 3) >> 2, qg = (my_q + 3) >> 2;
                 my_nb = mg * (mg + 1) / 2 + mg * qg;
                 my_sl = 4 * (mg + qg);
@@ -667,11 +687,7 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
                 M.sbase[i] = excl_s;
                 M.bbase[i] = excl_b;
                 M.obase[i] = co - (2 * my_m + my_q);
-                if (my_m > 0) {
-                    ++n_joins;
-                    n_m += my_m;
-                    n_q += my_q;
-                }
+                n_rows += my_m + my_q;
             }
             if (lane == 0) {
                 M.nnodes = nn;
@@ -722,12 +738,13 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
             n_joins += __shfl_xor_sync(kFull, n_joins, o);
             n_m += __shfl_xor_sync(kFull, n_m, o);
             n_q += __shfl_xor_sync(kFull, n_q, o);
+            n_rows += __shfl_xor_sync(kFull, n_rows, o);
         }
         if (lane == 0 && n_joins) {
             atomicAdd(&stats->joins, n_joins);
             atomicAdd(&stats->sum_m, n_m);
             atomicAdd(&stats->sum_q, n_q);
-            atomicAdd(&stats->rows, n_m + n_q);
+            atomicAdd(&stats->rows, n_rows);
         }
         return;
     }

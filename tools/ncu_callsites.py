@@ -38,6 +38,20 @@ with tempfile.TemporaryDirectory() as td:
                    cwd=td, capture_output=True)
     cubin = next(os.path.join(td, x) for x in os.listdir(td) if x.endswith(".cubin"))
     sass = subprocess.run(["nvdisasm", "-gi", cubin], capture_output=True, text=True).stdout.splitlines()
+if fn == "auto":
+    # the report's demangled kernel name -> the cubin's mangled one
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rr = list(csv.reader(io.StringIO(raw)))
+    want = rr[2][rr[0].index("Kernel Name")]
+    names = [l[len(".text."):-1] for l in sass if l.startswith(".text.") and l.endswith(":")]
+    dem = subprocess.run(["cu++filt"], input="\n".join(names), capture_output=True, text=True).stdout.splitlines()
+    def norm(x):  # name and template arguments only (ncu prints parameters as T1, ...)
+        x = re.sub(r"\((?:int|bool|unsigned int|long|unsigned long)\)", "", x).split("(")[0]
+        return re.sub(r"\s+|void|knng::|\(anonymous namespace\)::", "", x).replace("true", "1").replace("false", "0")
+    cand = [m for m, dm in zip(names, dem) if norm(dm) == norm(want)]
+    if not cand:
+        sys.exit(f"no cubin function matches {want!r}")
+    fn = cand[0]
 i0 = next(i for i, l in enumerate(sass) if l.startswith(".text." + fn + ":"))
 site = None
 sites = []
