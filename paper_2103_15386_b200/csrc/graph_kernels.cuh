@@ -130,6 +130,10 @@ __global__ void __launch_bounds__(256, 8) k_merge_sample(Dims D, Graph G, Sample
     const int k = D.k, p = D.p;
     const bool in_list = static_cast<int>(lane) < k;
     const uint32_t mask = G.newmask[s];
+    // the bucket's count and offset load with the list (one dependent
+    // global round trip less before the bucket itself)
+    const uint32_t bc = do_merge ? G.bcnt[s] : 0u;
+    const uint64_t bo = do_merge ? G.boff[s] : 0ull;
     Elem cur{in_list ? G.keys[static_cast<size_t>(s) * k + lane] : kSentinel,
              in_list ? ((mask >> lane) & 1u) : 0u};
     bool changed = false;
@@ -141,13 +145,13 @@ __global__ void __launch_bounds__(256, 8) k_merge_sample(Dims D, Graph G, Sample
         }
     }
     if (do_merge) {
-        const uint32_t c = G.bcnt[s];
+        const uint32_t c = bc;
         if (c > 0) {
             extern __shared__ uint64_t ms_scratch[];  // per warp: list copy, merged keys (64 u64), metas (32 u32)
             uint64_t* lst = ms_scratch + (threadIdx.x >> 5) * 80;
             uint64_t* outk = lst + 32;
             uint32_t* outm = reinterpret_cast<uint32_t*>(lst + 64);
-            const uint64_t* bk = G.bucket + G.boff[s];
+            const uint64_t* bk = G.bucket + bo;
             for (uint32_t base = 0; base < c; base += 32) {
                 const uint64_t cand = (base + lane < c) ? bk[base + lane] : kSentinel;
                 // Pre-filter (exact): a candidate equal to a list key is the
@@ -171,12 +175,32 @@ __global__ void __launch_bounds__(256, 8) k_merge_sample(Dims D, Graph G, Sample
                 // Merge by ranks (no sorting network): a survivor lands at
                 // (list entries below it) + (survivors below it); a list entry
                 // moves down by the survivors below it; past slot k: dropped.
-                int r = 0, sh = 0;
-                for (uint32_t rem = km; rem; rem &= rem - 1) {
-                    const uint64_t x = shfl_u64(cand, __ffs(rem) - 1);
-                    r += x < cand;
-                    sh += x < cur.key;
+                // No per-survivor loop: the list separates the survivors, so
+                // survivor x is below list entry i iff pos(x) <= i -- the
+                // shifts are the prefix counts of a histogram of the
+                // insertion positions, and a survivor's rank is the count
+                // below its position plus its rank among the (few) survivors
+                // sharing that position.  (The loop over survivors was 56 %
+                // of this kernel's instructions, profiles/r02e_ncu_k_merge_sample.txt.)
+                int* hist = reinterpret_cast<int*>(outm);  // outm / outk are free until the output step
+                uint64_t* sc = outk;
+                __syncwarp();
+                hist[lane] = 0;
+                sc[lane] = cand;
+                __syncwarp();
+                if (keep) atomicAdd(hist + pos, 1);
+                __syncwarp();
+                int sh = hist[lane];  // -> survivors with pos <= lane
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int t = __shfl_up_sync(kFull, sh, o);
+                    if (static_cast<int>(lane) >= o) sh += t;
                 }
+                const int below = __shfl_sync(kFull, sh, pos > 0 ? pos - 1 : 0);
+                int r = pos > 0 ? below : 0;
+                const uint32_t grp = __match_any_sync(kFull, keep ? static_cast<uint32_t>(pos) : 64u + lane);
+                if (keep)
+                    for (uint32_t g = grp & ~(1u << lane); g; g &= g - 1) r += sc[__ffs(g) - 1] < cand;
                 __syncwarp();
                 outk[lane] = kSentinel;
                 outm[lane] = 0u;

@@ -361,6 +361,11 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
     uint32_t f1_tgt = 0;
     uint64_t f2_key[2], f2_pos[2];
     uint32_t f2_tgt = 0;
+    // bucket mode: the slot returned by the count atomic is consumed only by
+    // the next iteration's stores, so the atomic's return latency is not
+    // waited for inside the iteration that issued it
+    uint64_t f2_bo = 0;
+    uint32_t f2_sl = 0, f2_ok0 = 0;
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
         f1_key[r] = kSentinel;
@@ -369,36 +374,38 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
     }
     unsigned long long n_cand = 0, n_app = 0, my_pairs = 0;
     auto file_store = [&]() {
+        if constexpr (REC) {  // record mode (distributed refine)
 #pragma unroll
-        for (int r = 0; r < 2; ++r)
-            if (f2_key[r] != kSentinel) {
-                if constexpr (REC) {  // record mode (distributed refine)
+            for (int r = 0; r < 2; ++r)
+                if (f2_key[r] != kSentinel) {
                     G.rec_key[f2_pos[r]] = f2_key[r];
                     G.rec_tgt[f2_pos[r]] = f2_tgt;
-                } else {
-                    G.bucket[f2_pos[r]] = f2_key[r];
                 }
-            }
+        } else {
+            const uint64_t p0 = f2_bo + f2_sl;
+            if (f2_key[0] != kSentinel) G.bucket[p0] = f2_key[0];
+            if (f2_key[1] != kSentinel) G.bucket[p0 + f2_ok0] = f2_key[1];
+        }
     };
     auto file_atomic = [&]() {
         const bool ok0 = f1_key[0] < f1_th, ok1 = f1_key[1] < f1_th;  // D17 (the sentinel never passes)
         n_app += ok0 + ok1;
-        uint64_t sl = 0;
         if constexpr (REC) {
             // record slots: one atomic per warp (the call is warp-uniform)
             const uint32_t b0 = __ballot_sync(kFull, ok0), b1 = __ballot_sync(kFull, ok1);
             unsigned long long wb = 0;
             if (lane == 0 && (b0 | b1)) wb = atomicAdd(G.rec_cnt, static_cast<unsigned long long>(__popc(b0) + __popc(b1)));
-            sl = shfl_u64(wb, 0) + __popc(b0 & lanemask_lt()) + __popc(b1 & lanemask_lt());
-            f1_bo = 0;
+            const uint64_t sl = shfl_u64(wb, 0) + __popc(b0 & lanemask_lt()) + __popc(b1 & lanemask_lt());
             f2_tgt = f1_tgt;
-        } else if (ok0 || ok1) {
-            sl = atomicAdd(G.bcnt + f1_tgt, static_cast<uint32_t>(ok0 + ok1));
+            f2_pos[0] = sl;
+            f2_pos[1] = sl + (ok0 ? 1 : 0);
+        } else {
+            f2_sl = (ok0 || ok1) ? atomicAdd(G.bcnt + f1_tgt, static_cast<uint32_t>(ok0 + ok1)) : 0u;
+            f2_bo = f1_bo;
+            f2_ok0 = ok0 ? 1u : 0u;
         }
         f2_key[0] = ok0 ? f1_key[0] : kSentinel;
-        f2_pos[0] = f1_bo + sl;
         f2_key[1] = ok1 ? f1_key[1] : kSentinel;
-        f2_pos[1] = f1_bo + sl + (ok0 ? 1 : 0);
         f1_key[0] = kSentinel;
         f1_key[1] = kSentinel;
         f1_th = 0;

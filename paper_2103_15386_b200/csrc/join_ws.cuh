@@ -62,10 +62,6 @@ struct WsMeta {
     int m[kWsMaxNodes], q[kWsMaxNodes], sbase[kWsMaxNodes], bbase[kWsMaxNodes + 1];
     int obase[kWsMaxNodes + 1];  // prefix of the 2m+q selected keys per node
     uint32_t ids[kWsSlots];
-    // node (index in the batch) of every 4x4 block and of every selected
-    // key: one shared load instead of a dependent search over the prefixes
-    uint8_t bnode[kWsBlocks];
-    uint8_t onode[2 * kWsSlots];
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -229,7 +225,7 @@ __device__ unsigned long long g_ws_prof[32];
 #define WS_T0(v) const long long v = clock64()
 #define WS_ACC(v, site)                                                                         \
     do {                                                                                        \
-        if ((WS_PROBE() & 32) && (threadIdx.x & 31) == 0)                                       \
+        if ((probe & 32) && (threadIdx.x & 31) == 0)                                            \
             atomicAdd(&g_ws_prof[site], static_cast<unsigned long long>(clock64() - (v)));      \
     } while (0)
 #else
@@ -239,14 +235,14 @@ __device__ unsigned long long g_ws_prof[32];
 #endif
 
 template <bool SUSP>
-__device__ __forceinline__ void ws_idle_wait(uint64_t* bar, uint32_t parity, int site = 31) {
+__device__ __forceinline__ void ws_idle_wait(uint64_t* bar, uint32_t parity, int site = 31, int probe = 0) {
 #ifdef KNNG_WS_PROF
     const long long t0 = clock64();
 #endif
     if constexpr (SUSP) mbar_wait_idle(bar, parity);
     else mbar_wait_sleep(bar, parity);
 #ifdef KNNG_WS_PROF
-    if ((WS_PROBE() & 32) && (threadIdx.x & 31) == 0)
+    if ((probe & 32) && (threadIdx.x & 31) == 0)
         atomicAdd(&g_ws_prof[site], static_cast<unsigned long long>(clock64() - t0));
 #endif
 }
@@ -320,11 +316,11 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
         unsigned long long n_cand = 0, n_app = 0;
         for (uint32_t b = g;; b += kWsEpiGroups) {
             const int mb = b % kWsMeta, pb = b & 1;
-            ws_idle_wait<Cfg::kPair>(mfull + mb, (b / kWsMeta) & 1, 0);
+            ws_idle_wait<Cfg::kPair>(mfull + mb, (b / kWsMeta) & 1, 0, probe);
             const WsMeta& M = meta[mb];
             const int nn = M.nnodes;
             if (nn == 0) break;
-            ws_idle_wait<Cfg::kPair>(pfull + pb, (b >> 1) & 1, 1);
+            ws_idle_wait<Cfg::kPair>(pfull + pb, (b >> 1) & 1, 1, probe);
             WS_T0(t_sel);
             const unsigned long long* rowp = parts + pb * 8 * kWsBlocks;
             const unsigned long long* colp = rowp + 4 * kWsBlocks;
@@ -336,7 +332,10 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
                 uint64_t v = kSentinel;
                 uint32_t tgt = 0;
                 if (o < total) {
-                    const int i = M.onode[o];
+                    int i = 0;  // the last node with obase[i] <= o
+#pragma unroll
+                    for (int step = 16; step > 0; step >>= 1)
+                        if (i + step < nn && M.obase[i + step] <= o) i += step;
                     const int j = o - M.obase[i];
                     const int mi = M.m[i], qi = M.q[i];
                     const int mgi = (mi + 3) >> 2, qgi = (qi + 3) >> 2, bb = M.bbase[i];
@@ -478,7 +477,7 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
                         if (i1 != 0xFFFFFFFFu) r1[i] = __ldg(reinterpret_cast<const float4*>(src + static_cast<size_t>(i1) * d));
                     }
                 }
-                ws_idle_wait<Cfg::kPair>(empty + st, ((slab_it / STAGES) & 1) ^ 1, 2);
+                ws_idle_wait<Cfg::kPair>(empty + st, ((slab_it / STAGES) & 1) ^ 1, 2, probe);
                 float* stage = reinterpret_cast<float*>(ring) + static_cast<size_t>(st) * (Cfg::kStageBytes / 4);
 #pragma unroll
                 for (int i = 0; i < kTaskPerThr; ++i) {
@@ -502,7 +501,7 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
             const int nslots = M.nslots;
             for (int sl = 0; sl < nslab; ++sl) {
                 const int st = slab_it % STAGES;
-                ws_idle_wait<Cfg::kPair>(empty + st, ((slab_it / STAGES) & 1) ^ 1, 3);
+                ws_idle_wait<Cfg::kPair>(empty + st, ((slab_it / STAGES) & 1) ^ 1, 3, probe);
                 const int e0 = sl * SD + part * CE;
                 E* dst = ring + static_cast<size_t>(st) * kWsSlots * RS;
                 const E* src0 = V + e0;
@@ -532,7 +531,7 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
         if (warp < kWsConsumerWarps + kWsGatherWarps) {  // gather warps follow the batch stream
             while (true) {
                 const int mb = meta_it % kWsMeta;
-                ws_idle_wait<Cfg::kPair>(mfull + mb, (meta_it / kWsMeta) & 1, 4);
+                ws_idle_wait<Cfg::kPair>(mfull + mb, (meta_it / kWsMeta) & 1, 4, probe);
                 const WsMeta& M = meta[mb];
                 if (M.nnodes == 0) break;
                 gather(M);
@@ -600,6 +599,7 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
         fetch(0, x0);
         int cur = 32;  // position inside the current 32-node chunk
         int my_m = 0, my_q = 0, my_nb = 0, my_sl = 0;
+        int p_nb = 0, p_sl = 0, p_co = 0;  // chunk prefix sums of blocks, slots, selected keys
         unsigned long long n_joins = 0, n_m = 0, n_q = 0, n_rows = 0;
         while (true) {
             if (cur >= 32) {
@@ -640,6 +640,23 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
                 const int mg = (my_m + 3) >> 2, qg = (my_q + 3) >> 2;
                 my_nb = mg * (mg + 1) / 2 + mg * qg;
                 my_sl = 4 * (mg + qg);
+                // inclusive prefix sums over the chunk's 32 nodes, once per
+                // chunk: a batch's bounds are then differences (no per-batch
+                // shuffle scans -- the lead's shuffles queue behind the
+                // consumers' shared-memory traffic)
+                p_nb = my_nb;
+                p_sl = my_sl;
+                p_co = 2 * my_m + my_q;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int tb = __shfl_up_sync(kFull, p_nb, o), ts = __shfl_up_sync(kFull, p_sl, o);
+                    const int tc = __shfl_up_sync(kFull, p_co, o);
+                    if (static_cast<int>(lane) >= o) {
+                        p_nb += tb;
+                        p_sl += ts;
+                        p_co += tc;
+                    }
+                }
                 cur = 0;
                 cur_buf = buf;
                 cur_x0 = x0;
@@ -649,45 +666,49 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
                 WS_ACC(t_chunk, 11);
             }
             // take nodes cur.. while the batch's blocks and slots fit
+            // bounds relative to the chunk prefix before node `cur`
+            const int src0 = cur > 0 ? cur - 1 : 0;
+            int b_nb = __shfl_sync(kFull, p_nb, src0), b_sl = __shfl_sync(kFull, p_sl, src0);
+            int b_co = __shfl_sync(kFull, p_co, src0);
+            if (cur == 0) b_nb = b_sl = b_co = 0;
             const bool pending = static_cast<int>(lane) >= cur;
-            int cb = pending ? my_nb : 0, cs = pending ? my_sl : 0;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int tb = __shfl_up_sync(kFull, cb, o), ts = __shfl_up_sync(kFull, cs, o);
-                if (static_cast<int>(lane) >= o) { cb += tb; cs += ts; }
-            }
-            const bool fits = pending && cb <= kWsBlocks && cs <= kWsSlots;
+            const bool fits = pending && p_nb - b_nb <= kWsBlocks && p_sl - b_sl <= kWsSlots;
             const uint32_t fm = __ballot_sync(kFull, fits);
             const int end = fm ? 32 - __clz(fm) : cur;  // fits is a prefix of [cur, 32)
-            const int nb_tot = __shfl_sync(kFull, cb, end - 1 < 0 ? 0 : end - 1);
-            const int ns_tot = __shfl_sync(kFull, cs, end - 1 < 0 ? 0 : end - 1);
+            const int src1 = end - 1 < 0 ? 0 : end - 1;
+            const int nb_tot = __shfl_sync(kFull, p_nb, src1) - b_nb;
+            const int ns_tot = __shfl_sync(kFull, p_sl, src1) - b_sl;
+            const int no_tot = __shfl_sync(kFull, p_co, src1) - b_co;
             const int first = cur;
             cur = end;
-            if (nb_tot == 0) continue;  // only nodes without NEW samples
-            // ---- publish batch metadata
+            if (end <= first || nb_tot == 0) continue;  // only nodes without NEW samples
+            // ---- publish batch metadata: every lane its own node (no
+            // per-node shuffles)
             const int mb = meta_it % kWsMeta;
-            ws_idle_wait<Cfg::kPair>(mempty + mb, ((meta_it / kWsMeta) & 1) ^ 1, 5);
+            ws_idle_wait<Cfg::kPair>(mempty + mb, ((meta_it / kWsMeta) & 1) ^ 1, 5, probe);
             WsMeta& M = meta[mb];
             WS_T0(t_pub);
             const int nn = end - first;
-            const int excl_b = cb - (pending ? my_nb : 0), excl_s = cs - (pending ? my_sl : 0);
             const bool in_batch = static_cast<int>(lane) >= first && static_cast<int>(lane) < end;
-            int co = in_batch ? 2 * my_m + my_q : 0;  // selected keys per node
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int tc = __shfl_up_sync(kFull, co, o);
-                if (static_cast<int>(lane) >= o) co += tc;
-            }
-            const int no_tot = __shfl_sync(kFull, co, end - 1);
             if (in_batch) {
                 const int i = lane - first;
+                const int sb = p_sl - my_sl - b_sl;
                 M.x[i] = cur_x0 + lane;
                 M.m[i] = my_m;
                 M.q[i] = my_q;
-                M.sbase[i] = excl_s;
-                M.bbase[i] = excl_b;
-                M.obase[i] = co - (2 * my_m + my_q);
+                M.sbase[i] = sb;
+                M.bbase[i] = p_nb - my_nb - b_nb;
+                M.obase[i] = p_co - (2 * my_m + my_q) - b_co;
                 n_rows += my_m + my_q;
+                // the sample ids of my slots, from the chunk cache
+                const uint32_t* row = cc_ids + static_cast<size_t>(cur_buf) * 32 * 2 * cap + lane * 2 * cap;
+                const int mpad = (my_m + 3) & ~3;
+                for (int js = 0; js < my_sl; ++js) {
+                    uint32_t id = 0xFFFFFFFFu;
+                    if (js < my_m) id = row[js];
+                    else if (js >= mpad && js - mpad < my_q) id = row[cap + (js - mpad)];
+                    M.ids[sb + js] = id;
+                }
             }
             if (lane == 0) {
                 M.nnodes = nn;
@@ -695,27 +716,6 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
                 M.nslots = ns_tot;
                 M.bbase[nn] = nb_tot;
                 M.obase[nn] = no_tot;
-            }
-            // node by node (values broadcast from the node's lane): the sample
-            // ids of its slots from the chunk cache, and its index in the
-            // block -> node and key -> node tables
-            const uint32_t* cids = cc_ids + static_cast<size_t>(cur_buf) * 32 * 2 * cap;
-            const int my_ob = co - (2 * my_m + my_q);
-            for (int i = 0; i < nn; ++i) {
-                const int src = first + i;
-                const int m = __shfl_sync(kFull, my_m, src), q = __shfl_sync(kFull, my_q, src);
-                const int sb = __shfl_sync(kFull, excl_s, src), bb = __shfl_sync(kFull, excl_b, src);
-                const int ob = __shfl_sync(kFull, my_ob, src);
-                const int mpad = (m + 3) & ~3, mg = mpad >> 2, qg = (q + 3) >> 2;
-                const uint32_t* row = cids + src * 2 * cap;
-                for (int js = lane; js < 4 * (mg + qg); js += 32) {
-                    uint32_t id = 0xFFFFFFFFu;
-                    if (js < m) id = row[js];
-                    else if (js >= mpad && js - mpad < q) id = row[cap + (js - mpad)];
-                    M.ids[sb + js] = id;
-                }
-                for (int t = lane; t < mg * (mg + 1) / 2 + mg * qg; t += 32) M.bnode[bb + t] = static_cast<uint8_t>(i);
-                for (int o = lane; o < 2 * m + q; o += 32) M.onode[ob + o] = static_cast<uint8_t>(i);
             }
             __syncwarp();
             WS_ACC(t_pub, 10);
@@ -727,7 +727,7 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
         // its own batch sequence); consumers and gatherers stop at the first
         for (int e = 0; e < kWsEpiGroups; ++e) {
             const int mb = meta_it % kWsMeta;
-            ws_idle_wait<Cfg::kPair>(mempty + mb, ((meta_it / kWsMeta) & 1) ^ 1, 6);
+            ws_idle_wait<Cfg::kPair>(mempty + mb, ((meta_it / kWsMeta) & 1) ^ 1, 6, probe);
             if (lane == 0) meta[mb].nnodes = 0;
             __syncwarp();
             mbar_arrive(mfull + mb);
@@ -756,13 +756,19 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
     for (uint32_t b = 0;; ++b) {
         const int mb = b % kWsMeta, pb = b & 1;
         if constexpr (Cfg::kPair) mbar_wait(mfull + mb, (b / kWsMeta) & 1);  // the critical role spins
-        else ws_idle_wait<false>(mfull + mb, (b / kWsMeta) & 1, 7);
+        else ws_idle_wait<false>(mfull + mb, (b / kWsMeta) & 1, 7, probe);
         const WsMeta& M = meta[mb];
         const int nn = M.nnodes;
         if (nn == 0) break;
         // ---- my block
         const bool active = ct < M.nblocks;
-        const int nd = active ? M.bnode[ct] : 0;
+        // my block's node: the last i with bbase[i] <= ct (binary search)
+        int nd = 0;
+        if (active) {
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1)
+                if (nd + step < nn && M.bbase[nd + step] <= ct) nd += step;
+        }
         const int m = M.m[nd], q = M.q[nd], sb = M.sbase[nd];
         const int mpad = (m + 3) & ~3, mg = mpad >> 2, qg = (q + 3) >> 2;
         const int t = ct - M.bbase[nd];
@@ -918,7 +924,7 @@ k_join_ws(const T* __restrict__ X, const float* __restrict__ Xn, Dims D, Graph G
         // ---- block minima: 4 row keys (c_nn / c_no candidates of the NEW
         // rows) and 4 column keys (c_nn / c_on candidates of the columns)
         if constexpr (Cfg::kPair) mbar_wait(pempty + pb, ((b >> 1) & 1) ^ 1);
-        else ws_idle_wait<false>(pempty + pb, ((b >> 1) & 1) ^ 1, 8);
+        else ws_idle_wait<false>(pempty + pb, ((b >> 1) & 1) ^ 1, 8, probe);
         unsigned long long* rowp = parts + pb * 8 * kWsBlocks;
         unsigned long long* colp = rowp + 4 * kWsBlocks;
         if (active) {
