@@ -438,6 +438,7 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
         xnext = static_cast<int64_t>(__shfl_sync(kFull, claim(), 0));
         claimed = claim();
         fetch(0, xnext);
+#ifndef KNNG_TC_LOCKSTEP
         for (uint32_t t = 0;; ++t) {
             const int slot = t % kTcPlans;
             if (t >= kTcPlans) mbar_wait_suspend(plan_empty + slot, ((t / kTcPlans) - 1) & 1);
@@ -446,9 +447,36 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
             if (lane == 0) mbar_arrive(plan_full + slot);
             if (last) break;
         }
+#else
+        // racecheck build (tools/racecheck_tc.sh): the same plans, but the
+        // planning warp also meets the epilogue warps at a CTA barrier once
+        // per batch (plan b+3 formed in iteration b), an ordering the race
+        // checker models -- the default build orders the same hand-offs
+        // with the plan_full / plan_empty mbarriers only
+        uint32_t last_t = 0xFFFFFFFFu;
+        auto form = [&](uint32_t t) {
+            const int slot = t % kTcPlans;
+            if (t >= kTcPlans) mbar_wait_suspend(plan_empty + slot, ((t / kTcPlans) - 1) & 1);
+            if (last_t == 0xFFFFFFFFu) {
+                form_plan(plans[slot]);
+                if (plans[slot].nnodes == 0) last_t = t;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(plan_full + slot);
+        };
+        for (uint32_t t = 0; t < 3; ++t) form(t);
+        named_bar(6, (PW + 1) * 32);
+        for (uint32_t b = 0; b < last_t; ++b) {
+            if (b + 3 <= last_t) form(b + 3);
+            named_bar(6, (PW + 1) * 32);
+        }
+#endif
     } else {
         // ---- warps 0-3: two batches of rows in flight
         bool ended = false;  // a terminator plan has been seen
+#ifdef KNNG_TC_LOCKSTEP
+        named_bar(6, (PW + 1) * 32);  // plans 0-2 formed
+#endif
         for (int t = 0; t < 2; ++t) {
             if (!ended) {
                 mbar_wait(plan_full + t, 0);
@@ -617,6 +645,9 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
                 mbar_arrive(plan_empty + slot);  // this warp is done with plan b
             }
             side_prev = side_next;
+#ifdef KNNG_TC_LOCKSTEP
+            named_bar(6, (PW + 1) * 32);
+#endif
         }
     }
     if (warp < PW && !upper) {

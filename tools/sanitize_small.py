@@ -10,7 +10,7 @@ import paper_2103_15386_b200.knng as K  # noqa: E402
 
 Xs = torch.from_numpy(datagen.make("sift", 3000, seed=3)).cuda()      # exact-u8 tensor-core join (TMA)
 Xd = torch.from_numpy(datagen.make("deep", 3000, seed=3)).cuda()      # float join
-for jk in [0, 7, 8]:
+for jk in [0, 2, 3]:
     K.knng_set_option("join_kernel", jk)
     K.knng_build(Xs, 16, 3, 8, 1)
     K.knng_build(Xd, 16, 3, 8, 1)
