@@ -297,9 +297,11 @@ knng_status knng_debug_philox(const uint32_t* ctr, int64_t m, uint64_t seed,
  *                     automatic choice for rows that are not 16-B aligned);
  *                  2: always the warp-specialised join (float rows: the
  *                     packed FP32x2 tile, FADD2/FFMA2 on pair-interleaved
- *                     stages);
+ *                     stages; the automatic choice for L2 and chi-square
+ *                     float rows);
  *                  3: the warp-specialised join with the scalar FP32 tile
- *                     (the previous float path, kept as the A/B reference);
+ *                     and cp.async row gathers (the automatic choice for
+ *                     cosine);
  *                  4: float rows (L2 / cosine, d % 4 == 0, d <= 128): the
  *                     TF32 tensor-core join (join_tcf.cuh) -- exact
  *                     selection by canonical recomputation inside an

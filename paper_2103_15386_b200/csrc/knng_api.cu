@@ -621,9 +621,25 @@ struct Run {
         if (al && !force_v3) {
             // warp-specialised pipeline (bulk row copies need 16-B aligned,
             // 16-B multiple row slabs)
-            constexpr int STG = 4;   // 32-KB stages (row-slab layout: u8, option 3)
-            constexpr int STP = 4;   // 33-KB stages (pair-interleaved layout of the packed FP32x2 tile)
-            const bool pk = jk != 3;  // option 3: the scalar FP32 tile (A/B reference point)
+#ifndef WS_STG
+#define WS_STG 3
+#endif
+#ifndef WS_STP
+#define WS_STP 2
+#endif
+            // Fewer stages are faster: the shared memory they leave to L1
+            // serves the row gathers (rows recur across nearby batches) --
+            // DEEP 1M packed: 10.1 (4 stages) -> 9.2 (3) -> 9.1 ms (2);
+            // scalar: 10.4 (5) -> 9.7 (4) -> 9.65 ms (3)
+            // (tools/ws_stage_variants.sh, profiles/r02_float_join_ab.txt)
+            constexpr int STG = WS_STG;  // 32-KB stages (row-slab layout: u8 and the scalar float tile)
+            constexpr int STP = WS_STP;  // 33-KB stages (pair-interleaved layout of the packed FP32x2 tile)
+            // float tile: the packed FP32x2 tile for L2 (DEEP-shaped 9.1 vs
+            // 9.65 ms per launch, GIST-shaped 10.4 vs 11.8 ms) and
+            // chi-square, the scalar tile for cosine (8.1 vs 8.5 ms: its
+            // one FMA per dimension leaves the packed tile no issue slots to
+            // save) -- profiles/r02_float_join_ab.txt.  Options 2 / 3 force one.
+            const bool pk = jk == 2 || (jk != 3 && metric != KNNG_COSINE);
             unsigned long long* work = reinterpret_cast<unsigned long long*>(ws + L.flag + 8);
             cudaMemsetAsync(work, 0, 8, c.stream);
             const float* Xf = static_cast<const float*>(X);
