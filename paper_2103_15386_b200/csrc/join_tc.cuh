@@ -51,7 +51,10 @@ constexpr int kTcWarps = 5;      // 4 epilogue/gather + 1 planning
 constexpr int kTcThreads = kTcWarps * 32;
 constexpr int kTcPlanWarp = 4;
 constexpr int kTcCtasPerSm = 4;  // 4 x 128 TMEM columns
-constexpr int kTcPlans = 4;      // plan ring: b (scan), b+1, b+2 (rows in flight), b+3 (being formed)
+#ifndef TC_PLANS
+#define TC_PLANS 4
+#endif
+constexpr int kTcPlans = TC_PLANS;  // plan ring: b (scan), b+1, b+2 (rows in flight), b+3.. (being formed)
 
 struct TcPlan {
     int nnodes;  // 0 = no more work
@@ -73,7 +76,7 @@ struct TcCfg {
     static constexpr size_t kCombOff = (kBarOff + 8 * (1 + 2 * kTcPlans + 2) + 8 + 15) & ~size_t(15);
     static constexpr size_t kUsed = kCombOff + 2 * kTcRows * 4;  // + upper-half partial minima (EPI = 8)
     static constexpr size_t kSmem = kUsed + 1024;  // + slack to align the rows to 1024 B
-    static_assert(kTcCtasPerSm * (kSmem + 1024) <= 233472, "4 CTAs per SM");
+    static_assert((kTcPlans > 4 ? 3 : kTcCtasPerSm) * (kSmem + 1024) <= 233472, "CTAs per SM");
 };
 
 // SW128 K-major shared-memory matrix descriptor (tcgen05): rows of 128 B,
@@ -117,6 +120,23 @@ __device__ __forceinline__ void mbar_wait_suspend(uint64_t* bar, uint32_t parity
         "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
         "r"(parity), "r"(1000000)
         : "memory");
+}
+// 0xFFFFFFFF << sh with the PTX clamp (sh >= 32 -> 0; unsigned, so a
+// negative amount also gives 0)
+__device__ __forceinline__ uint32_t shl_ones(uint32_t sh) {
+    uint32_t r;
+    asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(0xFFFFFFFFu), "r"(sh));
+    return r;
+}
+__device__ __forceinline__ uint32_t shl_clamp(uint32_t x, uint32_t sh) {
+    uint32_t r;
+    asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(sh));
+    return r;
+}
+// bits [a, b) of a 32-bit word for a <= b (a, b any ints): two clamped
+// shifts, no branches
+__device__ __forceinline__ uint32_t bit_range_fast(int a, int b) {
+    return shl_ones(static_cast<uint32_t>(max(a, 0))) & ~shl_ones(static_cast<uint32_t>(max(b, 0)));
 }
 // bits [a, b) of a 32-bit word, clamped
 __device__ __forceinline__ uint32_t bit_range(int a, int b) {
@@ -534,6 +554,16 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
             const int lo = act ? sb : kTcRows;
             const int hi = act ? (isNEW ? sb + m + q : sb + m) : 0;
             const int wlo = __reduce_min_sync(kFull, lo), whi = __reduce_max_sync(kFull, hi);
+            // row masks as ranges: A = [alo, ahi) (the node's NEW columns,
+            // scanned by NEW and OLD rows), B = [blo, bhi) (its OLD columns,
+            // NEW rows only); empty ranges have lo = hi
+            const int alo = act ? sb : 0, ahi = act ? sb + m : 0;
+            const int blo = isNEW ? sb + m : 0, bhi = isNEW ? sb + m + q : 0;
+            const uint32_t selfbit = isNEW ? 1u : 0u;
+            // distance evaluations of the method (m(m-1)/2 + m q per join):
+            // the NEW row of rank i pairs with the i NEW rows before it and
+            // the q OLD rows -- closed form unless a GGM refine masks pairs
+            if (!restricted && isNEW && !upper) my_pairs += (s - sb) + q;
             const uint32_t my_id = P.ids[s];
             const bool myside = restricted && static_cast<int64_t>(my_id) >= boundary;
             const int nbuf = b % 3;  // norms/sides: b (scan), b+1, b+2 (staged by other warps meanwhile)
@@ -551,7 +581,11 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
             // ---- MMA(b) has read rows[buf]: gather batch b+2 into it
             if (!ended) {
                 const int s2 = (b + 2) % kTcPlans;
+#ifdef TC_SUSPEND
+                mbar_wait_suspend(plan_full + s2, ((b + 2) / kTcPlans) & 1);
+#else
                 mbar_wait(plan_full + s2, ((b + 2) / kTcPlans) & 1);
+#endif
                 ended = plans[s2].nnodes == 0;
             }
             if (!ended) gather(plans[(b + 2) % kTcPlans], rows + buf * TcCfg::kRowBytes);
@@ -565,9 +599,8 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
             const int cs = upper ? c0 + 16 * half : c0;
             const int ce = upper ? whi : min(whi, c0 + 16 * half);
             for (int cb = cs; cb < ce; cb += 16) {
-                uint32_t A = act ? bit_range(sb - cb, sb + m - cb) : 0u;
-                if (isNEW && s >= cb && s < cb + 16) A &= ~(1u << (s - cb));
-                uint32_t B = isNEW ? bit_range(sb + m - cb, sb + m + q - cb) : 0u;
+                uint32_t A = bit_range_fast(alo - cb, ahi - cb) & ~shl_clamp(selfbit, static_cast<uint32_t>(s - cb));
+                uint32_t B = bit_range_fast(blo - cb, bhi - cb);
                 if (restricted) {
                     const uint32_t sd = side[nbuf * 4 + (cb >> 5)] >> (cb & 16);
                     const uint32_t allow = myside ? ~sd : sd;
@@ -581,7 +614,7 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
                 tc_ld16(tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + cb, r);
                 A &= 0xFFFFu;
                 B &= 0xFFFFu;
-                if (isNEW) my_pairs += __popc(A & bit_range(0, s - cb)) + __popc(B);
+                if (restricted && isNEW) my_pairs += __popc(A & ~shl_ones(static_cast<uint32_t>(max(s - cb, 0)))) + __popc(B);
                 const int4* nv4 = reinterpret_cast<const int4*>(nb + cb);
                 int kk[16];
 #pragma unroll
