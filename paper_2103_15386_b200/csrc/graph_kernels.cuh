@@ -166,12 +166,23 @@ __global__ void __launch_bounds__(256, 8) k_merge_sample(Dims D, Graph G, Sample
                 for (int step = 16; step > 0; step >>= 1)
                     if (lst[pos + step - 1] < cand) pos += step;
                 bool keep = cand < kth && lst[pos] != cand;
-                // repeated candidates (the same key from two joins): the lowest lane stays
                 const uint32_t km0 = __ballot_sync(kFull, keep);
                 if (km0 == 0) continue;
-                const uint32_t same = __match_any_sync(kFull, keep ? cand : kSentinel);
-                keep = keep && (same & km0 & lanemask_lt()) == 0u;
-                const uint32_t km = __ballot_sync(kFull, keep);
+                int* hist = reinterpret_cast<int*>(outm);  // outm / outk are free until the output step
+                uint64_t* sc = outk;
+                __syncwarp();
+                hist[lane] = 0;
+                sc[lane] = cand;
+                __syncwarp();
+                // candidates sharing an insertion position (one 32-bit match);
+                // equal keys (the same candidate from two joins) always share
+                // it: the lowest lane of each key stays
+                const uint32_t grp = __match_any_sync(kFull, keep ? static_cast<uint32_t>(pos) : 64u + lane);
+                const uint32_t others = keep ? (grp & ~(1u << lane)) : 0u;
+                bool dup = false;
+                for (uint32_t g = others & lanemask_lt(); g; g &= g - 1) dup |= sc[__ffs(g) - 1] == cand;
+                const uint32_t dupm = __ballot_sync(kFull, dup);
+                keep = keep && !dup;
                 // Merge by ranks (no sorting network): a survivor lands at
                 // (list entries below it) + (survivors below it); a list entry
                 // moves down by the survivors below it; past slot k: dropped.
@@ -182,12 +193,6 @@ __global__ void __launch_bounds__(256, 8) k_merge_sample(Dims D, Graph G, Sample
                 // below its position plus its rank among the (few) survivors
                 // sharing that position.  (The loop over survivors was 56 %
                 // of this kernel's instructions, profiles/r02e_ncu_k_merge_sample.txt.)
-                int* hist = reinterpret_cast<int*>(outm);  // outm / outk are free until the output step
-                uint64_t* sc = outk;
-                __syncwarp();
-                hist[lane] = 0;
-                sc[lane] = cand;
-                __syncwarp();
                 if (keep) atomicAdd(hist + pos, 1);
                 __syncwarp();
                 int sh = hist[lane];  // -> survivors with pos <= lane
@@ -198,9 +203,8 @@ __global__ void __launch_bounds__(256, 8) k_merge_sample(Dims D, Graph G, Sample
                 }
                 const int below = __shfl_sync(kFull, sh, pos > 0 ? pos - 1 : 0);
                 int r = pos > 0 ? below : 0;
-                const uint32_t grp = __match_any_sync(kFull, keep ? static_cast<uint32_t>(pos) : 64u + lane);
                 if (keep)
-                    for (uint32_t g = grp & ~(1u << lane); g; g &= g - 1) r += sc[__ffs(g) - 1] < cand;
+                    for (uint32_t g = others & ~dupm; g; g &= g - 1) r += sc[__ffs(g) - 1] < cand;
                 __syncwarp();
                 outk[lane] = kSentinel;
                 outm[lane] = 0u;
