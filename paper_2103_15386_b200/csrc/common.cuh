@@ -124,6 +124,31 @@ __device__ __forceinline__ uint32_t warp_sort_u32(uint32_t x) {
     }
     return x;
 }
+// Bitonic sort of every block of P lanes (P = 2, 4, ..., 32, a compile-time
+// constant), ascending: with data in lanes [0, P) and 0xFFFFFFFF above, the
+// whole warp is ascending after log2(P) phases instead of 5.
+template <int P>
+__device__ __forceinline__ uint32_t warp_sort_u32_blocks(uint32_t x) {
+    const uint32_t lane = lane_id();
+    uint32_t m_prev = 0;
+#pragma unroll
+    for (int k2 = 2; k2 <= P; k2 <<= 1) {
+        const uint32_t m = (k2 < P && (lane & k2)) ? 0xFFFFFFFFu : 0u;
+        x ^= m ^ m_prev;
+        m_prev = m;
+#pragma unroll
+        for (int j = k2 >> 1; j > 0; j >>= 1) {
+            const uint32_t o = __shfl_xor_sync(kFull, x, j);
+            x = (lane & j) ? max(o, x) : min(o, x);
+        }
+    }
+    return x;
+}
+// ascending sort of lanes [0, n) (0xFFFFFFFF above; n warp-uniform): the
+// 16-lane network when the data fits it
+__device__ __forceinline__ uint32_t warp_sort_u32_n(uint32_t x, int n) {
+    return n <= 16 ? warp_sort_u32_blocks<16>(x) : warp_sort_u32(x);
+}
 // bitonic sequence across the warp -> ascending
 __device__ __forceinline__ uint64_t warp_bitonic_merge_u64(uint64_t x) {
     const uint32_t lane = lane_id();

@@ -27,15 +27,18 @@
 // order is the id order (k_rev_select writes both sample lists sorted, D11).
 // With n'_c = n_c * 128 + c staged per batch, one IMAD per column forms it.
 //
-// CTA = 4 epilogue/gather warps + 1 planning warp; 4 CTAs per SM, each with
-// 128 TMEM columns.  The planning warp fills a 4-deep plan ring (mbarrier
-// hand-off) from the chunk cache, running ahead of the rest.  Iteration b of
-// warps 0-3 (two row buffers, two batches of rows in flight):
-//     wait rows(b); proxy fence; named barrier
-//     thread 0: kch MMAs (K = 32 each) of batch b -> TMEM, commit -> mbarrier
-//     wait MMA(b) -> rows[b & 1] is free: cp.async rows(b+2) into it (SW128
-//       K-major layout) and load their norms
-//     filing of b-1 / b-2 (as join_ls) while MMA(b) runs
+// CTA = EPI epilogue warps (4, or 8 in the default instance: 3 CTAs per SM)
+// + 1 planning warp, 128 TMEM columns per CTA.  The planning warp fills a
+// 4-deep plan ring (mbarrier hand-off) from the chunk cache, running ahead of
+// the rest, and (TMA build, TC_PGATHER) issues each batch's row gathers once
+// the MMA two batches back has released the row buffer.  Iteration b of the
+// epilogue warps (two row buffers, two batches of rows in flight):
+//     named barrier (TMEM reads of b-1 done, norms of b visible)
+//     thread 0: wait rows(b); kch MMAs (K = 32 each) of batch b -> TMEM,
+//       commit -> mbarrier(s)
+//     filing of b-1 / b-2 while MMA(b) runs
+//     wait MMA(b); load the norms of batch b+2 (cp.async build: also copy
+//       rows(b+2) into the freed buffer, SW128 K-major layout)
 //     row scans of b (tcgen05.ld); keys of b and their targets' loads
 #pragma once
 #include <climits>
@@ -51,6 +54,16 @@ constexpr int kTcWarps = 5;      // 4 epilogue/gather + 1 planning
 constexpr int kTcThreads = kTcWarps * 32;
 constexpr int kTcPlanWarp = 4;
 constexpr int kTcCtasPerSm = 4;  // 4 x 128 TMEM columns
+// TC_PGATHER: the planning warp issues the TMA row gathers of each batch
+// (after the MMA two batches back has released the row buffer, signalled by
+// a second tcgen05.commit) instead of 4 lanes of every epilogue warp
+#ifndef TC_PGATHER
+#define TC_PGATHER 1
+#endif
+#ifdef KNNG_TC_LOCKSTEP
+#undef TC_PGATHER
+#define TC_PGATHER 0
+#endif
 #ifndef TC_PLANS
 #define TC_PLANS 4
 #endif
@@ -73,7 +86,7 @@ struct TcCfg {
     static constexpr size_t kCacheCnt = 2 * 64;
     static constexpr size_t kCacheBytes = kCacheCnt + 2 * 32 * 2 * 32 * sizeof(uint32_t);
     static constexpr size_t kBarOff = (kCacheOff + kCacheBytes + 7) & ~size_t(7);
-    static constexpr size_t kCombOff = (kBarOff + 8 * (1 + 2 * kTcPlans + 2) + 8 + 15) & ~size_t(15);
+    static constexpr size_t kCombOff = (kBarOff + 8 * (1 + 2 * kTcPlans + 4) + 8 + 15) & ~size_t(15);
     static constexpr size_t kUsed = kCombOff + 2 * kTcRows * 4;  // + upper-half partial minima (EPI = 8)
     static constexpr size_t kSmem = kUsed + 1024;  // + slack to align the rows to 1024 B
     static_assert((kTcPlans > 4 ? 3 : kTcCtasPerSm) * (kSmem + 1024) <= 233472, "CTAs per SM");
@@ -151,8 +164,8 @@ __device__ __forceinline__ uint32_t bit_range(int a, int b) {
 // the same TMEM lane quarter and split the row's column chunks, the upper
 // half handing its partial minima over through shared memory; 3 CTAs per SM
 // then keep 24 epilogue warps resident instead of 16.
-// TMA: rows gathered by tcgen05-era TMA gather4 (one instruction per 4 rows,
-// issued by warp 0) instead of 16-B cp.async copies by every thread.
+// TMA: rows gathered by TMA gather4 (one instruction per 4 rows, issued by
+// the planning warp) instead of 16-B cp.async copies by every thread.
 // REC: record mode of the distributed refine (dist_kernels.cuh) -- a template
 // parameter, so the single-GPU build carries no per-key mode branch (the
 // runtime check cost ~10 % of this kernel: 2.47 -> 2.73 ms per C2 launch).
@@ -175,7 +188,8 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
     uint64_t* plan_full = mma_bar + 1;             // [kTcPlans] planning warp -> warps 0-3
     uint64_t* plan_empty = plan_full + kTcPlans;   // [kTcPlans] warps 0-3 -> planning warp
     uint64_t* rows_full = plan_empty + kTcPlans;  // [2] TMA row gathers of buffer 0 / 1
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rows_full + 2);
+    uint64_t* rows_free = rows_full + 2;          // [2] MMA done reading buffer 0 / 1 (TC_PGATHER)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rows_free + 2);
     int* comb = reinterpret_cast<int*>(tc_smem + TcCfg::kCombOff);
     constexpr int PW = EPI;  // the planning warp
 
@@ -331,7 +345,9 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
     auto gather = [&](const TcPlan& P, uint8_t* dst) {
         const int nslots = P.nslots;  // hoisted: the asm below clobbers memory
         const uint32_t dbase = smem_u32(dst);
-        if constexpr (TMA) {
+        if constexpr (TMA && TC_PGATHER) {
+            // (rows issued by the planning warp)
+        } else if constexpr (TMA) {
             // group g of 4 slots is issued by lane g % 4 of warp g / 4 (the
             // tx count may run ahead of the expect_tx: it is signed)
             const int ng = (nslots + 3) >> 2;  // groups of 4 slots; the tail repeats a valid row
@@ -442,6 +458,8 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
         mbar_init(mma_bar, 1);
         mbar_init(rows_full, 1);
         mbar_init(rows_full + 1, 1);
+        mbar_init(rows_free, 1);
+        mbar_init(rows_free + 1, 1);
         for (int i = 0; i < kTcPlans; ++i) {
             mbar_init(plan_full + i, 1);
             mbar_init(plan_empty + i, PW);
@@ -466,6 +484,23 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
             const bool last = plans[slot].nnodes == 0;
             if (lane == 0) mbar_arrive(plan_full + slot);
             if (last) break;
+            if constexpr (TMA && TC_PGATHER) {
+                // rows of batch t into buffer t & 1 once MMA(t-2) has read it
+                const int rb = t & 1;
+                if (t >= 2) mbar_wait_suspend(rows_free + rb, ((t - 2) >> 1) & 1);
+                const TcPlan& P = plans[slot];
+                const int nslots = P.nslots, ng = (nslots + 3) >> 2;
+                uint64_t* bar = rows_full + rb;
+                if (lane == 0) mbar_expect_tx(bar, static_cast<uint32_t>(ng) * 512u);
+                if (static_cast<int>(lane) < ng) {
+                    const int s0 = 4 * static_cast<int>(lane);
+                    const int r0 = static_cast<int>(P.ids[s0]);
+                    const int r1 = s0 + 1 < nslots ? static_cast<int>(P.ids[s0 + 1]) : r0;
+                    const int r2 = s0 + 2 < nslots ? static_cast<int>(P.ids[s0 + 2]) : r0;
+                    const int r3 = s0 + 3 < nslots ? static_cast<int>(P.ids[s0 + 3]) : r0;
+                    tma_gather4(rows + rb * TcCfg::kRowBytes + s0 * 128, &tmap, r0, r1, r2, r3, bar);
+                }
+            }
         }
 #else
         // racecheck build (tools/racecheck_tc.sh): the same plans, but the
@@ -517,7 +552,8 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
                 side_prev = side_next;
             }
         }
-        for (uint32_t b = 0;; ++b) {
+        uint32_t b = 0;
+        for (;; ++b) {
             const int slot = b % kTcPlans;
             const TcPlan& P = plans[slot];
             const int buf = b & 1;
@@ -536,6 +572,7 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
                     tc_mma_i8(tmem, desc, desc, k > 0 ? 1u : 0u);
                 }
                 tc_commit(mma_bar);
+                if constexpr (TMA && TC_PGATHER) tc_commit(rows_free + buf);
             }
 
             // ---- my row of batch b
@@ -681,6 +718,12 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
 #ifdef KNNG_TC_LOCKSTEP
             named_bar(6, (PW + 1) * 32);
 #endif
+        }
+        if constexpr (TMA && TC_PGATHER) {
+            // the row-buffer releases of the last two batches have landed
+            // before the shared memory goes away
+            if (tid == 0)
+                for (uint32_t l = b > 2 ? b - 2 : 0; l < b; ++l) mbar_wait(rows_free + (l & 1), (l >> 1) & 1);
         }
     }
     if (warp < PW && !upper) {
