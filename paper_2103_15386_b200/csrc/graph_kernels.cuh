@@ -354,12 +354,42 @@ __global__ void k_rev_scatter(Dims D, Samples S) {
     S.rsrc[static_cast<size_t>(f) * S.rstride + S.off[f * (D.n + 1) + v] + pos] = static_cast<uint32_t>(s);
 }
 
+// The same, 4 forward samples per thread (p % 4 == 0): the 4 targets' CSR
+// offsets are loaded together, so 4 dependent random reads are in flight per
+// thread instead of one.
+__global__ void k_rev_scatter4(Dims D, Samples S) {
+    const int f = blockIdx.y;
+    const int64_t i4 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // group of 4 samples
+    const int64_t q = D.p >> 2;
+    if (i4 >= D.n * q) return;
+    const int64_t s = i4 / q;
+    const int j0 = static_cast<int>(i4 - s * q) * 4;
+    const int fc = S.fcnt[2 * s + f];
+    if (j0 >= fc) return;
+    const size_t at = static_cast<size_t>(f) * D.n * D.p + static_cast<size_t>(s) * D.p + j0;
+    const uint4 v = *reinterpret_cast<const uint4*>(S.fwd + at);
+    uint32_t* rs = S.rsrc + static_cast<size_t>(f) * S.rstride;
+    const int cnt = min(4, fc - j0);
+    const uint32_t src = static_cast<uint32_t>(s);
+    const uint4 pos = *reinterpret_cast<const uint4*>(S.fpos + at);
+    const uint64_t* off = S.off + f * (D.n + 1);
+    uint64_t o0 = off[v.x], o1 = 0, o2 = 0, o3 = 0;
+    if (cnt > 1) o1 = off[v.y];
+    if (cnt > 2) o2 = off[v.z];
+    if (cnt > 3) o3 = off[v.w];
+    rs[o0 + pos.x] = src;
+    if (cnt > 1) rs[o1 + pos.y] = src;
+    if (cnt > 2) rs[o2 + pos.z] = src;
+    if (cnt > 3) rs[o3 + pos.w] = src;
+}
+
 // sort + dedup one u32 id per lane (0xFFFFFFFF = empty, sorts last); returns
 // the unique sorted ids compacted to lanes [0, count) and sets count.
-// scratch: 32 u32 of per-warp shared memory (compaction by rank scatter).
-__device__ __forceinline__ uint32_t warp_sort_unique_ids(uint32_t id, int& count, uint32_t* scratch) {
+// n: occupied lanes are [0, n) (warp-uniform; the sort runs on blocks of the
+// next power of two).  scratch: 32 u32 of per-warp shared memory.
+__device__ __forceinline__ uint32_t warp_sort_unique_ids(uint32_t id, int& count, uint32_t* scratch, int n = 32) {
     const uint32_t lane = lane_id();
-    const uint32_t x = warp_sort_u32(id);
+    const uint32_t x = warp_sort_u32_n(id, n);
     const uint32_t prev = __shfl_sync(kFull, x, (lane + 31) & 31);
     const bool ok = x != 0xFFFFFFFFu && (lane == 0 || x != prev);
     const uint32_t okm = __ballot_sync(kFull, ok);
@@ -387,7 +417,7 @@ __device__ __forceinline__ bool rev_select_ties(uint32_t src, int r, int f, uint
             philox4x32_10(make_uint4(f == 0 ? kTagRevNew : kTagRevOld, tword, src, static_cast<uint32_t>(v)), key);
         pr = (o.x & ~31u) | lane;  // (v: the node's id, D.base + local index)
     }
-    pr = warp_sort_u32(pr);
+    pr = warp_sort_u32_n(pr, r);
     const uint32_t prev = __shfl_sync(kFull, pr, (lane + 31) & 31);
     const bool tie = lane > 0 && static_cast<int>(lane) < r && (pr >> 5) == (prev >> 5);
     if (__any_sync(kFull, tie)) return true;
@@ -468,7 +498,7 @@ __global__ void __launch_bounds__(256, 8) k_rev_select(Dims D, Samples S, uint32
             if (j >= 0 && j < c) e = static_cast<uint32_t>(got);
         }
         int cnt = 0;
-        uint32_t u = warp_sort_unique_ids(e, cnt, scr);
+        uint32_t u = warp_sort_unique_ids(e, cnt, scr, max(1, fc + min(r, c)));
         if (f == 0) {
             gnew = u;
             m = cnt;

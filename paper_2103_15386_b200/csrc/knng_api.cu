@@ -51,6 +51,10 @@ knng_status fail(knng_status s, const char* fmt, ...) {
 }
 
 constexpr int kMaxIters = 256;
+#ifndef KNNG_REV_SCATTER4
+#define KNNG_REV_SCATTER4 1
+#endif
+constexpr bool g_rev_scatter4 = KNNG_REV_SCATTER4 != 0;
 
 // ---------------------------------------------------------------- layout
 struct Layout {
@@ -505,7 +509,10 @@ struct Run {
         });
         const int64_t items = D.n * D.p;
         c.launch("k_rev_scatter", [&] {
-            k_rev_scatter<<<dim3(static_cast<unsigned>((items + 255) / 256), 2), 256, 0, c.stream>>>(D, S);
+            if (D.p % 4 == 0 && g_rev_scatter4)
+                k_rev_scatter4<<<dim3(static_cast<unsigned>((items / 4 + 255) / 256), 2), 256, 0, c.stream>>>(D, S);
+            else
+                k_rev_scatter<<<dim3(static_cast<unsigned>((items + 255) / 256), 2), 256, 0, c.stream>>>(D, S);
         });
         const int wpb = 8;
         c.launch("k_rev_select", [&] {
