@@ -286,7 +286,10 @@ def measure_ggm(args, K, Xd, stream):
             "join_ms_per_launch": join_ms / max(1, join_launches),
             "dist_evals": sum(s["dist_evals"] for s in st), "accepted": sum(s["accepted"] for s in st),
             "dist_evals_per_s": sum(s["dist_evals"] for s in st) / (ms * 1e-3),
-            "kernel_ms_per_merge": kernels}
+            "kernel_ms_per_merge": kernels,
+            # device time of the merge's own kernels (the events above also
+            # see the host between the blocking calls)
+            "kernel_sum_ms_per_merge": round(sum(kernels.values()), 3)}
 
 
 FP32_ISSUE_PEAK = None  # set from the SM count and the sampled clock
