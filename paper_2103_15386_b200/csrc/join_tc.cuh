@@ -64,6 +64,9 @@ constexpr int kTcCtasPerSm = 4;  // 4 x 128 TMEM columns
 #undef TC_PGATHER
 #define TC_PGATHER 0
 #endif
+#ifndef TC_PMIN
+#define TC_PMIN 1
+#endif
 #ifndef TC_PLANS
 #define TC_PLANS 4
 #endif
@@ -665,6 +668,28 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
                 // masked minima, 3-input VIMNMX3; a mask that is empty on
                 // every lane of the warp (OLD rows, chunks outside the OLD
                 // range) is skipped as a whole
+#if TC_PMIN
+                // predicated minima (one IMNMX per selected element, the
+                // predicates unpacked from the mask by R2P), two chains
+                if (__any_sync(kFull, A != 0u)) {
+                    int a1 = INT_MAX;
+#pragma unroll
+                    for (int e = 0; e < 16; e += 2) {
+                        if ((A >> e) & 1u) minA = min(minA, kk[e]);
+                        if ((A >> (e + 1)) & 1u) a1 = min(a1, kk[e + 1]);
+                    }
+                    minA = min(minA, a1);
+                }
+                if (__any_sync(kFull, B != 0u)) {
+                    int b1 = INT_MAX;
+#pragma unroll
+                    for (int e = 0; e < 16; e += 2) {
+                        if ((B >> e) & 1u) minB = min(minB, kk[e]);
+                        if ((B >> (e + 1)) & 1u) b1 = min(b1, kk[e + 1]);
+                    }
+                    minB = min(minB, b1);
+                }
+#else
                 if (__any_sync(kFull, A != 0u)) {
 #pragma unroll
                     for (int e = 0; e < 16; e += 2)
@@ -677,6 +702,7 @@ k_join_tc(const uint8_t* __restrict__ X, const int* __restrict__ sqn, Dims D, Gr
                         minB = __vimin3_s32(minB, (B >> e) & 1u ? kk[e] : INT_MAX,
                                             (B >> (e + 1)) & 1u ? kk[e + 1] : INT_MAX);
                 }
+#endif
             }
             tc_fence_before();
             if constexpr (EPI == 8) {
