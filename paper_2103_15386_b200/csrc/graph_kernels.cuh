@@ -613,6 +613,38 @@ __global__ void k_check_nonneg(const float* __restrict__ X, int64_t total, int* 
     if (__syncthreads_or(!ok) && threadIdx.x == 0) atomicExch(bad, 1);
 }
 
+// option exact_u8, fused: one warp per row (d % 4 == 0, 16-B aligned rows)
+// checks that every value is an integer in [0, 255], writes the uint8 copy
+// and the row's exact squared norm (the tensor-core join's n_c) in one pass
+// over the float rows; bad = 1 if any value fails (the copy is then unused)
+__global__ void k_to_u8_checked(const float* __restrict__ X, int64_t n, int d, uint8_t* __restrict__ Y,
+                                int* __restrict__ sqn, int* bad) {
+    const uint32_t lane = lane_id();
+    const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    bool ok = true;
+    for (int64_t row = w0; row < n; row += nw) {
+        const float4* x = reinterpret_cast<const float4*>(X + row * d);
+        uchar4* y = reinterpret_cast<uchar4*>(Y + row * d);
+        int acc = 0;
+        for (int j = static_cast<int>(lane); j < (d >> 2); j += 32) {
+            const float4 v = __ldg(x + j);
+            ok &= v.x >= 0.0f && v.x <= 255.0f && v.x == rintf(v.x);
+            ok &= v.y >= 0.0f && v.y <= 255.0f && v.y == rintf(v.y);
+            ok &= v.z >= 0.0f && v.z <= 255.0f && v.z == rintf(v.z);
+            ok &= v.w >= 0.0f && v.w <= 255.0f && v.w == rintf(v.w);
+            const uchar4 u = make_uchar4(static_cast<uint8_t>(v.x), static_cast<uint8_t>(v.y),
+                                         static_cast<uint8_t>(v.z), static_cast<uint8_t>(v.w));
+            y[j] = u;
+            acc += u.x * u.x + u.y * u.y + u.z * u.z + u.w * u.w;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+        if (lane == 0) sqn[row] = acc;
+    }
+    if (__any_sync(kFull, !ok) && lane == 0) atomicExch(bad, 1);
+}
+
 __global__ void k_u8_to_f32(const uint8_t* __restrict__ X, int64_t total, float* __restrict__ Y) {
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)

@@ -51,6 +51,9 @@ knng_status fail(knng_status s, const char* fmt, ...) {
 }
 
 constexpr int kMaxIters = 256;
+#ifndef KNNG_FUSED_U8
+#define KNNG_FUSED_U8 1
+#endif
 #ifndef KNNG_REV_SCATTER4
 #define KNNG_REV_SCATTER4 1
 #endif
@@ -386,13 +389,28 @@ struct Run {
         int* flag = reinterpret_cast<int*>(ws + L.flag);
         const int64_t total = D.n * D.d;
         cudaMemsetAsync(flag, 0, 4, c.stream);
+        uint8_t* xu8 = reinterpret_cast<uint8_t*>(ws + L.xu8);
+        if (KNNG_FUSED_U8 && D.d % 4 == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 && xrows < 0 && !sqn_ext) {
+            // check, convert and the exact squared norms in one pass
+            int* sqn = reinterpret_cast<int*>(ws + L.sqn);
+            c.launch("k_to_u8", [&] {
+                k_to_u8_checked<<<8 * sms, 256, 0, c.stream>>>(static_cast<const float*>(X), D.n, D.d, xu8, sqn, flag);
+            });
+            int h = 1;
+            cudaMemcpyAsync(&h, flag, 4, cudaMemcpyDeviceToHost, c.stream);
+            if (cudaStreamSynchronize(c.stream) != cudaSuccess || h) return;
+            X = xu8;
+            dt = KNNG_U8;
+            sqn_ready = true;
+            g_last_exact_u8 = 1;
+            return;
+        }
         c.launch("k_check_u8", [&] {
             k_check_u8<<<4 * sms, 256, 0, c.stream>>>(static_cast<const float*>(X), total, flag);
         });
         int h = 1;
         cudaMemcpyAsync(&h, flag, 4, cudaMemcpyDeviceToHost, c.stream);
         if (cudaStreamSynchronize(c.stream) != cudaSuccess || h) return;
-        uint8_t* xu8 = reinterpret_cast<uint8_t*>(ws + L.xu8);
         c.launch("k_to_u8", [&] {
             k_to_u8<<<4 * sms, 256, 0, c.stream>>>(static_cast<const float*>(X), total, xu8);
         });
