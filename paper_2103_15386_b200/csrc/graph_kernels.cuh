@@ -65,9 +65,13 @@ __device__ __forceinline__ uint32_t kmask_of(int k) { return k >= 32 ? kFull : (
 // Alg. 1 lines 1-4: k distinct random ids != s (D1, D2) drawn in
 // counter order j = 0, 1, ... from Philox(INIT, s, j, s >> 32), canonical
 // distances, sorted by key (D3), all NEW.
+// do_sample: also the first iteration's sampling step (k_merge_sample with
+// no merge, fused): every entry is NEW, so FN(s) = the first min(p, k)
+// entries (marked OLD, each counted in its target's reverse list), FO(s) is
+// empty (D7, D12-D13).
 template <typename T, int MET>
 __global__ void k_init(const T* __restrict__ X, const float* __restrict__ Xn, Dims D,
-                       uint64_t seed, Graph G) {
+                       uint64_t seed, Graph G, Samples S, int do_sample) {
     const int64_t s = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (s >= D.n) return;
     const uint32_t lane = lane_id();
@@ -110,8 +114,22 @@ __global__ void k_init(const T* __restrict__ X, const float* __restrict__ Xn, Di
     }
     kk = warp_sort_u64(kk);
     if (static_cast<int>(lane) < k) G.keys[static_cast<size_t>(s) * k + lane] = kk;
-    if (lane == 0) G.newmask[s] = kmask_of(k);
     if (static_cast<int>(lane) == k - 1) G.kth[s] = kk;
+    if (!do_sample) {
+        if (lane == 0) G.newmask[s] = kmask_of(k);
+        return;
+    }
+    const int p = D.p, fn = min(p, k);
+    if (static_cast<int>(lane) < fn) {
+        const uint32_t id = key_id(kk);
+        S.fwd[static_cast<size_t>(s) * p + lane] = id;
+        S.fpos[static_cast<size_t>(s) * p + lane] = atomicAdd(S.rcnt + id, 1u);
+    }
+    if (lane == 0) {
+        G.newmask[s] = kmask_of(k) & ~kmask_of(fn);
+        S.fcnt[2 * s] = static_cast<uint8_t>(fn);
+        S.fcnt[2 * s + 1] = 0;
+    }
 }
 
 // ---------------------------------------------------- list update + sample

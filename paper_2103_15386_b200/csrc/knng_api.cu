@@ -51,6 +51,9 @@ knng_status fail(knng_status s, const char* fmt, ...) {
 }
 
 constexpr int kMaxIters = 256;
+#ifndef KNNG_FUSED_INIT
+#define KNNG_FUSED_INIT 1
+#endif
 #ifndef KNNG_FUSED_U8
 #define KNNG_FUSED_U8 1
 #endif
@@ -434,9 +437,14 @@ struct Run {
             k_init_seg<uint8_t, kMetL2, SEG><<<grid, wpb * 32, sm, c.stream>>>(static_cast<const uint8_t*>(X), nullptr, D, seed, G);
     }
 
-    void init() {
+    // with_sample: fuse the first iteration's sampling step into k_init
+    // (one-segment lists, local reverse counts; iteration 0 then skips it)
+    bool init_sampled = false;
+    void init(bool with_sample = false) {
         const int wpb = 8;
         const int grid = warps_grid(D.n, wpb);
+        const int do_sample = with_sample && KNNG_FUSED_INIT && segs() == 1 && S.fpos != nullptr && !G.imask ? 1 : 0;
+        init_sampled = do_sample != 0;
         if (segs() > 1) {  // segmented lists (D40)
             c.launch("k_init", [&] {
                 if (segs() == 2) init_seg<2>(grid, wpb);
@@ -447,13 +455,13 @@ struct Run {
         }
         c.launch("k_init", [&] {
             if (metric == KNNG_COSINE)
-                k_init<float, true><<<grid, wpb * 32, wpb * 32 * 4, c.stream>>>(nullptr, Xn, D, seed, G);
+                k_init<float, true><<<grid, wpb * 32, wpb * 32 * 4, c.stream>>>(nullptr, Xn, D, seed, G, S, do_sample);
             else if (metric == KNNG_CHI2)
-                k_init<float, kMetChi2><<<grid, wpb * 32, wpb * 32 * 4, c.stream>>>(static_cast<const float*>(X), nullptr, D, seed, G);
+                k_init<float, kMetChi2><<<grid, wpb * 32, wpb * 32 * 4, c.stream>>>(static_cast<const float*>(X), nullptr, D, seed, G, S, do_sample);
             else if (dt == KNNG_F32)
-                k_init<float, false><<<grid, wpb * 32, wpb * 32 * 4, c.stream>>>(static_cast<const float*>(X), nullptr, D, seed, G);
+                k_init<float, false><<<grid, wpb * 32, wpb * 32 * 4, c.stream>>>(static_cast<const float*>(X), nullptr, D, seed, G, S, do_sample);
             else
-                k_init<uint8_t, false><<<grid, wpb * 32, wpb * 32 * 4, c.stream>>>(static_cast<const uint8_t*>(X), nullptr, D, seed, G);
+                k_init<uint8_t, false><<<grid, wpb * 32, wpb * 32 * 4, c.stream>>>(static_cast<const uint8_t*>(X), nullptr, D, seed, G, S, do_sample);
         });
     }
 
@@ -733,7 +741,7 @@ struct Run {
     }
 
     void iteration(int iter, uint32_t tword, bool merge_first) {
-        merge_sample(merge_first ? 1 : 0, 1, merge_first ? iter - 1 : -1);
+        if (!(iter == 0 && init_sampled)) merge_sample(merge_first ? 1 : 0, 1, merge_first ? iter - 1 : -1);
         reverse(tword);
         if (!join(iter)) scatter(iter);
     }
@@ -844,7 +852,7 @@ knng_status knng_build(const void* vectors, knng_dtype dt, int64_t n, int32_t d,
     R.zero_state();
     if ((s = R.normalize())) return s;
     R.compress();
-    R.init();
+    R.init(true);
     for (int t = 0; t < iters; ++t) R.iteration(t, static_cast<uint32_t>(t), t > 0);
     R.merge_sample(1, 0, iters - 1);
     R.export_graph(out_ids, out_dists);
